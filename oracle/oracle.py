@@ -1,0 +1,189 @@
+"""CPU ORACLE for the LARS gradient-combine-and-update step — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` / ``--impl
+reference`` legs may import this module. The product path (``paper_1903_12650_b200``) never
+imports, links or executes it, and this module imports nothing from the product path.
+
+Plain, slow, obviously correct float64 NumPy following the paper's method step by step
+(SURVEY.md §8(c) O1-O8). Passages followed (arxiv 1903.12650, /root/reference/PAPER.md):
+
+  * PAPER.md:29-31 (§I)       "the weight gradients from all processes are combined to update
+                               all the weights"                                   -> combine()
+  * PAPER.md:96-98 (§III-A-1) warm-up "which raises learning rate gradually"      -> lr_at()
+  * PAPER.md:99-100, 78-80    LARS "adjusts the learning rate of each layer according to the
+                               norms weight and gradient"                         -> trust_ratio()
+  * PAPER.md:102-103          decay patterns "step, polynomial, linear"           -> lr_at()
+  * PAPER.md:130-135 (§III-B-2) per-layer norms for LARS                          -> l2norm()
+  * PAPER.md:183 (§IV)        "compute and communicate using half precision ... update own
+                               weights using single precision"                    -> to_double()
+  * PAPER.md:184-185          "original optimizer ... warmup and LARS"            -> step()
+  * PAPER.md:210-211          1,280,000 images / 81,920 batch -> 16 updates per epoch, 1,440
+                               in total                                           -> schedule()
+
+Where the paper is silent, the readings of SURVEY.md §8(c) are used and listed in DESIGN.md
+§"Readings": LARS form lambda = eta*||w||/(||g|| + beta*||w|| + eps) (#1), lr*lambda inside the
+velocity (#2), lambda = 1 fallback (#3), bias/BN skip kinds (#4), linear warm-up lr(t) =
+base*(t+1)/W (#6), W = round-half-up(warmup_epochs*ipe) (#7), polynomial decay toward 0 over
+[W,T) (#8), ipe = ceil(D/B) (#11), sum then multiply by grad_scale (#12), whole-step skip on a
+non-finite norm (#13), lr(t) for the update performed at iteration t (#21).
+
+Every function here is pinned by ``tests/test_oracle_pins.py``.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+WEIGHT, BIAS, BN_GAMMA, BN_BETA = "weight", "bias", "bn_gamma", "bn_beta"
+
+
+@dataclass
+class HParams:
+    base_lr: float
+    eta: float = 1e-3
+    momentum: float = 0.9
+    weight_decay: float = 5e-5
+    eps: float = 0.0
+    warmup_epochs: float = 5.0
+    poly_power: float = 2.0
+    global_batch: int = 81920
+    dataset_size: int = 1_280_000
+    total_epochs: int = 90         # PAPER.md:211; log epochs 0..89
+    grad_scale: float = 1.0
+
+
+# ----------------------------------------------------------------------------------------------
+# O1. Schedule
+# ----------------------------------------------------------------------------------------------
+def iterations_per_epoch(dataset_size: int, global_batch: int) -> int:
+    """ipe = ceil(D / B): "the number of updates in an epoch is only 16"."""
+    return -(-dataset_size // global_batch)
+
+
+def schedule(hp: HParams) -> tuple[int, int, int]:
+    """(ipe, T, W): T = E * ipe (1,440 at B=81,920); W in iterations (reading #7)."""
+    ipe = iterations_per_epoch(hp.dataset_size, hp.global_batch)
+    T = hp.total_epochs * ipe
+    W = int(math.floor(hp.warmup_epochs * ipe + 0.5))
+    return ipe, T, W
+
+
+def lr_at(hp: HParams, t: int) -> float:
+    """Learning rate for the update performed at iteration t (0-based).
+
+    Warm-up (reading #6): base * (t+1) / W for t < W.
+    Polynomial decay (reading #8): base * (1 - (t-W)/(T-W))^p for W <= t < T,
+    evaluated as base * ((T-t)/(T-W))^p — the same number, written without the cancellation of
+    1 - (t-W)/(T-W) near t = T-1 (one rounding in the ratio instead of two).
+    """
+    _, T, W = schedule(hp)
+    if not (0 <= t < T):
+        raise ValueError(f"iteration {t} outside [0, {T})")
+    if t < W:
+        return hp.base_lr * (t + 1) / W
+    return hp.base_lr * ((T - t) / (T - W)) ** hp.poly_power
+
+
+# ----------------------------------------------------------------------------------------------
+# O2. Combine
+# ----------------------------------------------------------------------------------------------
+def to_double(g) -> np.ndarray:
+    """Half/single precision wire values -> float64 (exact). bf16 arrives as uint16 bit patterns."""
+    g = np.asarray(g)
+    if g.dtype == np.uint16:  # bf16 bit patterns: the high half of an IEEE single
+        return (g.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    return g.astype(np.float64)
+
+
+def combine(g_ranks: list, grad_scale: float) -> np.ndarray:
+    """G = s * sum_r g_r, summed in ascending rank order in float64."""
+    total = np.zeros(np.asarray(g_ranks[0]).shape, dtype=np.float64)
+    for g in g_ranks:
+        total = total + to_double(g)
+    return grad_scale * total
+
+
+# ----------------------------------------------------------------------------------------------
+# O3. Norms
+# ----------------------------------------------------------------------------------------------
+def l2norm(x: np.ndarray) -> float:
+    """sqrt of the correctly rounded sum of squares (math.fsum)."""
+    x = np.asarray(x, dtype=np.float64)
+    try:
+        return math.sqrt(math.fsum((x * x).tolist()))
+    except (OverflowError, ValueError):
+        s = float(np.sum(x * x))
+        return s if not math.isfinite(s) else math.sqrt(s)
+
+
+# ----------------------------------------------------------------------------------------------
+# O4. Trust ratio (reading #1, #3, #4)
+# ----------------------------------------------------------------------------------------------
+def trust_ratio(w_norm: float, g_norm: float, kind: str, eta: float, weight_decay: float,
+                eps: float) -> tuple[float, float]:
+    """Returns (lambda_l, beta_l). Skip kinds: (1, 0)."""
+    if kind != WEIGHT:
+        return 1.0, 0.0
+    denom = g_norm + weight_decay * w_norm + eps
+    if w_norm > 0.0 and denom > 0.0:
+        return eta * w_norm / denom, weight_decay
+    return 1.0, weight_decay
+
+
+# ----------------------------------------------------------------------------------------------
+# O5-O7. The step
+# ----------------------------------------------------------------------------------------------
+@dataclass
+class StepResult:
+    w: list            # float64 per tensor
+    m: list            # float64 per tensor
+    w_norm: list       # ||w_l||
+    g_norm: list       # ||G_l|| (G = s * sum_r g_r)
+    lam: list          # lambda_l
+    lr: float
+    skipped: bool
+    m_env: list = field(default_factory=list)  # magnitude envelopes (tolerance reading #17)
+    w_env: list = field(default_factory=list)
+
+
+def step(kinds: list, hp: HParams, t: int, w: list, g_ranks: list, m: list) -> StepResult:
+    """One LARS momentum-SGD update at iteration t.
+
+    kinds:   per-tensor kind strings
+    w, m:    per-tensor float32 (or float64) arrays — master weights / momentum
+    g_ranks: g_ranks[r][l] = rank r's gradient for tensor l (fp16/bf16-bits/fp32)
+    """
+    lr = lr_at(hp, t)
+    L = len(kinds)
+    W64 = [np.asarray(x, dtype=np.float64) for x in w]
+    M64 = [np.asarray(x, dtype=np.float64) for x in m]
+    G = [combine([g_ranks[r][l] for r in range(len(g_ranks))], hp.grad_scale) for l in range(L)]
+    absg = [abs(hp.grad_scale) * sum(np.abs(to_double(g_ranks[r][l])) for r in range(len(g_ranks)))
+            for l in range(L)]
+    w_norm = [l2norm(W64[l]) for l in range(L)]
+    g_norm = [l2norm(G[l]) for l in range(L)]
+    lam, beta = zip(*[trust_ratio(w_norm[l], g_norm[l], kinds[l], hp.eta, hp.weight_decay, hp.eps)
+                      for l in range(L)]) if L else ((), ())
+
+    # O5: any non-finite norm -> the whole step is skipped (reading #13)
+    if not all(math.isfinite(x) for x in w_norm + g_norm):
+        return StepResult([x.copy() for x in W64], [x.copy() for x in M64], w_norm, g_norm,
+                          list(lam), lr, True)
+
+    w_new, m_new, m_env, w_env = [], [], [], []
+    for l in range(L):
+        u = G[l] + beta[l] * W64[l]                       # g + beta*w
+        v = hp.momentum * M64[l] + lr * lam[l] * u         # v <- mu*v + lr*lambda*(g + beta*w)
+        w_new.append(W64[l] - v)                           # w <- w - v
+        m_new.append(v)
+        m_env.append(abs(hp.momentum) * np.abs(M64[l])
+                     + abs(lr * lam[l]) * (absg[l] + abs(beta[l]) * np.abs(W64[l])))
+        w_env.append(np.abs(W64[l]) + np.abs(v))
+    return StepResult(w_new, m_new, w_norm, g_norm, list(lam), lr, False, m_env, w_env)
+
+
+def dp_step(kinds: list, hp: HParams, t: int, w: list, g_ranks: list, m: list) -> StepResult:
+    """O8: P simulated ranks. The data-parallel result is O1-O7 with the exact rank sum."""
+    return step(kinds, hp, t, w, g_ranks, m)
