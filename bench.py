@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""bench.py — ResNet-50 allreduce+LARS step: ms/step and params/s at N B200s, HBM / NVLink roofline.
+
+Workloads (BASELINE.json):
+  N = 1  configs[1]  "resnet50_f32_lars_step_1gpu": 161 tensors, 25,557,032 params, fp32 gradients,
+                     lars_step (K1 norms + K2 fused update) on one B200.
+  N > 1  configs[2]  "resnet50_f16_rs_lars_ag_dp{N}": fp16 gradients, NCCL reduce-scatter + sharded
+                     LARS update + fp32 weight all-gather (dp_allreduce_lars_step), one process per GPU.
+
+value = gradient elements combined and applied per second over the whole job: every rank contributes a
+full local gradient of 25,557,032 params per step (data parallelism), so a step processes
+N x 25,557,032 params; per-GPU work is fixed as N grows ("weak"). ms_per_step is the max over ranks.
+Inputs stay resident in HBM for `value`; `e2e` copies each step's gradient from pinned host memory
+(H2D) and reads the step status + per-layer norms back (D2H) inside the timed region.
+
+`--impl reference` times the float64 CPU oracle (oracle/oracle.py) on the host cores — the only other
+place bench.py executes oracle code besides the `cpu_baseline` leg.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ResNet-50 allreduce+LARS step ms & params/s at 1/2/4/8 B200; HBM/NVLink GB/s"
+NVLINK_PEER_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+HP = dict(base_lr=32.0, eta=1e-3, momentum=0.9, weight_decay=5e-5, eps=0.0, warmup_epochs=5.0, poly_power=2.0,
+          global_batch=81920)
+T0 = 719  # mid-schedule start iteration (t cycles through the 1,440-step schedule)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--soak-s", type=float, default=1.5, help="untimed steps while clocks settle/sampling")
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--layout", default="resnet50")
+    return ap.parse_args()
+
+
+def workload_name(P: int, layout: str) -> str:
+    return f"{layout}_f32_lars_step_1gpu" if P == 1 else f"{layout}_f16_rs_lars_ag_dp{P}"
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the measured region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.lines, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------------- ours
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1903_12650_b200 as PK
+    from synth import gen as G
+    from synth import layouts as LY
+
+    rank, P = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", args.gpus))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    assert P == args.gpus, f"WORLD_SIZE={P} but --gpus {args.gpus}"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if P > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    dtype = "f32" if P == 1 else "f16"
+    lay = LY.by_name(args.layout)
+    E = sum(t.numel for t in lay)
+    h = PK.Lars([(t.numel, t.kind) for t in lay], device=local, grad_dtype=dtype, nranks=P,
+                grad_scale=1.0 / (G.GRAD_PRESCALE * P), **HP)
+    if P > 1:
+        h.comm_init_torch()
+    gbytes = 4 if dtype == "f32" else 2
+
+    def dev_flat(arrs):
+        flat = G.pack(arrs, h.offsets, h.padded_numel)
+        return torch.from_numpy(flat).to(dev)
+
+    w_host, g_host, m_host = G.weights(lay), G.grads(lay, rank, 0, dtype), G.momentum(lay, 1e-3)
+    w, g, m = dev_flat(w_host), dev_flat(g_host), dev_flat(m_host)
+    T = h.total_iters
+    step = h.lars_step if P == 1 else h.dp_allreduce_lars_step
+    stream = torch.cuda.current_stream()
+    k = 0
+
+    def run(n):
+        nonlocal k
+        for _ in range(n):
+            step(w, g, m, (T0 + k) % T, stream)
+            k += 1
+
+    def barrier():
+        if P > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if P == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    run(args.warmup)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    t_end = time.time() + args.soak_s
+    while time.time() < t_end:
+        run(20)
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    run(args.steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms_total = max_over_ranks(e0.elapsed_time(e1))
+    assert not h.last_step_skipped(), "a timed step was skipped (non-finite) — invalid timing"
+    ms_step = ms_total / args.steps
+
+    # per-phase device times (library CUDA events on the same stream; separate pass)
+    nprof = min(args.steps, 200)
+    h.profile_enable(True)
+    barrier()
+    run(nprof)
+    phases, nsteps = h.profile_read()
+    h.profile_enable(False)
+    ph = {kk: max_over_ranks(v / max(1, nsteps)) for kk, v in phases.items()}
+
+    # end to end through the public API with host gradients
+    g_pin = torch.from_numpy(G.pack(g_host, h.offsets, h.padded_numel)).pin_memory()
+    step_h = h.lars_step_host_grad if P == 1 else h.dp_allreduce_lars_step_host_grad
+    ne = max(1, args.e2e_steps)
+    step_h(w, g_pin, m, T0 % T, stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for i in range(ne):
+        step_h(w, g_pin, m, (T0 + i) % T, stream)
+    e3.record(stream)
+    torch.cuda.synchronize()
+    skipped = h.last_step_skipped()
+    assert not skipped
+    ms_e2e = max_over_ranks(e2.elapsed_time(e3)) / ne
+    h2d = h.padded_numel * gbytes
+    d2h = 4 + 2 * 8 * (len(lay) if P == 1 else sum(1 for o in h.tensor_owner() if o == rank))
+
+    units = P * E
+    value = units / (ms_step * 1e-3)
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs")
+    peak_note = "measured (MEASURED_PEAKS.json hbm_gbs)" if hbm else "fallback (B200_PROFILING.md 6.65 TB/s)"
+    hbm = hbm or 6650.0
+    shard_elems = sum(t.numel for t, o in zip(lay, h.tensor_owner()) if o == rank)
+    upd_bytes = (4 + gbytes + 4 + 4 + 4) * shard_elems          # read w, g, m; write w, m
+    norm_bytes = (4 + gbytes) * shard_elems                      # read w, g
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            ns = json.load(f).get(workload_name(P, args.layout), {})
+        traffic = ns.get("update_dram_bytes")
+    except (OSError, ValueError):
+        pass
+    if P == 1:
+        ach = upd_bytes / (ph["update"] * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": "lars_update_kernel (K2)", "achieved": round(ach, 1), "peak": hbm,
+                "unit": "GB/s", "frac": round(ach / hbm, 4), "traffic": traffic,
+                "algorithmic_bytes_per_launch": upd_bytes, "launch_ms": round(ph["update"], 5),
+                "peak_source": peak_note}
+    else:
+        bus = (P - 1) / P * (gbytes + 4) * h.padded_numel
+        coll_ms = ph["reduce_scatter"] + ph["all_gather"]
+        ach = bus / (coll_ms * 1e-3) / 1e9
+        roof = {"bound": "nvlink", "kernel": "NCCL reduce-scatter + all-gather (C1+C2)", "achieved": round(ach, 1),
+                "peak": NVLINK_PEER_GBS, "unit": "GB/s", "frac": round(ach / NVLINK_PEER_GBS, 4), "traffic": None,
+                "bus_bytes_per_step": int(bus), "peak_source": "measured peer copy per direction, B200_PROFILING.md",
+                "step_frac_of_bus_roofline": round(bus / NVLINK_PEER_GBS / 1e9 / (ms_step * 1e-3), 4)}
+    step_alg = (upd_bytes) / (ms_step * 1e-3) / 1e9
+    out = {
+        "metric": METRIC, "value": round(value, 1), "unit": "params/s", "n_gpus": P, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "grad_dtype": dtype, "data": "synthetic",
+        "config": {"workload": workload_name(P, args.layout), "layout": args.layout, "tensors": len(lay),
+                   "params": E, "global_batch": HP["global_batch"], "iters": f"t=({T0}+k) mod {T}",
+                   "parallelism": f"dp{P}", "units": f"{P} x {E} gradient params combined+applied per step",
+                   "l2": f"inputs larger than L2: w+g+m = {(8 + gbytes) * h.padded_numel / 1e6:.0f} MB > 126 MB, "
+                         "no flush"},
+        "phases_ms": {kk: round(v, 5) for kk, v in ph.items() if v > 0},
+        "roofline": roof,
+        "roofline_step": {"bound": "hbm", "achieved": round(step_alg, 1), "peak": hbm, "unit": "GB/s",
+                          "frac": round(step_alg / hbm, 4),
+                          "note": "algorithmic update bytes (w,g,m read; w,m write) / whole step time"},
+        "e2e": {"value": round(units / (ms_e2e * 1e-3), 1), "unit": "params/s", "ms_per_step": round(ms_e2e, 4),
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "clocks": clk,
+        "gpu_launches": 2 * args.steps,
+        "nccl_launches": (3 * args.steps) if P > 1 else 0,
+    }
+    if P == 1 and rank == 0 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(lay, w_host, [g_host], m_host, dtype, P)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if P > 1:
+        dist.destroy_process_group()
+    del np
+
+
+def cpu_baseline(lay, w, g_ranks, m, dtype, P):
+    """The oracle, as it stands, on the host: one full ResNet-50 step (bounded ~10-30 s), 1 core."""
+    from oracle import oracle as O
+    from synth import gen as G
+
+    hp = O.HParams(grad_scale=1.0 / (G.GRAD_PRESCALE * P), **HP)
+    kinds = [t.kind for t in lay]
+    t0 = time.perf_counter()
+    O.step(kinds, hp, T0, w, g_ranks, m)
+    dt = time.perf_counter() - t0
+    E = sum(t.numel for t in lay)
+    return {"value": round(P * E / dt, 1), "unit": "params/s", "cores": 1, "kind": "oracle",
+            "sample": f"1 full {len(lay)}-tensor step ({E} params, {dtype} grads) in {dt:.2f} s, "
+                      f"single-threaded NumPy float64 + math.fsum"}
+
+
+# ----------------------------------------------------------------------------------------- reference
+def run_reference(args):
+    rank, P = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", args.gpus))
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from synth import gen as G
+    from synth import layouts as LY
+
+    dtype = "f32" if P == 1 else "f16"
+    lay = LY.by_name(args.layout)
+    E = sum(t.numel for t in lay)
+    hp = O.HParams(grad_scale=1.0 / (G.GRAD_PRESCALE * P), **HP)
+    # calibrate on the first few tensors, then size a contiguous tensor prefix so the whole run is bounded
+    cal = lay[:40]
+    wc, gc, mc = G.weights(cal), [G.grads(cal, r, 0, dtype) for r in range(P)], G.momentum(cal, 1e-3)
+    t0 = time.perf_counter()
+    O.step([t.kind for t in cal], hp, T0, wc, gc, mc)
+    rate = sum(t.numel for t in cal) / (time.perf_counter() - t0)
+    budget_s = 120.0
+    want = max(200_000, min(E, int(rate * budget_s / max(1, args.steps + args.warmup))))
+    n, acc = 0, 0
+    while n < len(lay) and acc < want:
+        acc += lay[n].numel
+        n += 1
+    sub = lay[:n]
+    w, m = G.weights(sub), G.momentum(sub, 1e-3)
+    g = [G.grads(sub, r, 0, dtype) for r in range(P)]
+    kinds = [t.kind for t in sub]
+    for i in range(args.warmup):
+        O.step(kinds, hp, (T0 + i) % 1440, w, g, m)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        O.step(kinds, hp, (T0 + i) % 1440, w, g, m)
+    dt = time.perf_counter() - t0
+    value = P * acc * args.steps / dt
+    sample = (f"first {n} of {len(lay)} tensors ({acc} of {E} params), {P} rank gradient(s) of {dtype}, "
+              f"per step; single-threaded NumPy float64 + math.fsum")
+    out = {"impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": "params/s", "n_gpus": P,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "grad_dtype": dtype,
+           "data": "synthetic",
+           "config": {"workload": workload_name(P, args.layout), "layout": args.layout, "tensors": len(lay),
+                      "params": E, "global_batch": HP["global_batch"], "parallelism": f"dp{P}",
+                      "units": f"{P} x sampled params per step"},
+           "cpu_baseline": {"value": round(value, 1), "unit": "params/s", "cores": 1, "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": round(value, 1), "unit": "params/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,188 @@
+/*
+ * lars.h — C ABI of the B200-native LARS gradient-combine-and-update library.
+ *
+ * The operation (arxiv 1903.12650, /root/reference/PAPER.md):
+ *   * data-parallel gradients "are combined to update all the weights"         PAPER.md:29-31 (§I)
+ *   * warm-up "which raises learning rate gradually"                           PAPER.md:96-98 (§III-A-1)
+ *   * LARS "adjusts the learning rate of each layer according to the norms
+ *     weight and gradient"
+ *   * decay patterns "step, polynomial, linear"
+ *   * "special GPU kernel for batched norm computations"                        PAPER.md:130-135 (§III-B-2)
+ *   * gradients "gathered" into multi-megabyte allreduces                       PAPER.md:147-153 (§III-C-1)
+ *   * "compute and communicate using half precision ... update own weights
+ *     using single precision"; "original optimizer"; warm-up + LARS            PAPER.md:183-185 (§IV)
+ *   * 1,280,000 images / 81,920 batch -> 16 updates per epoch, 1,440 in total   PAPER.md:210-211 (§IV)
+ *
+ * For iteration t (0-based) and every tensor l of the layout (readings in DESIGN.md §Readings):
+ *   G      = s * sum_r g_r                                 (s = hp.grad_scale; sum over P ranks)
+ *   lr(t)  = base*(t+1)/W  (t < W);  base*((T-t)/(T-W))^p  (W <= t < T)
+ *   lambda = eta*||w_l|| / (||G_l|| + beta*||w_l|| + eps)  for weight-kind tensors when ||w_l|| > 0
+ *            and the denominator > 0; otherwise 1.  Skip kinds (bias, BN gamma/beta): lambda = 1, beta_l = 0.
+ *   v      <- mu*v + lr(t)*lambda*(G + beta_l*w);   w <- w - v
+ *   If any ||w_l|| or ||G_l|| is non-finite the whole step is skipped: w and m are left bitwise unchanged.
+ *
+ * Conventions for every entry point:
+ *   * Pointers named w, g, m are CUDA DEVICE pointers on the handle's device unless the name ends in _host.
+ *   * Flat buffers hold `padded_numel` elements (lars_layout); tensor l lives at elements
+ *     [offsets[l], offsets[l] + numel_l). Offsets are library-assigned (64-element aligned), so
+ *     segments never overlap. Padding elements are never read or written by lars_step.
+ *   * w and m are float32 (master weights and momentum); g is hp.grad_dtype.
+ *   * Base pointers must be 256-byte aligned, else LARS_ERR_ALIGNMENT.
+ *   * The caller owns w, g, m. The library owns its scratch (work lists, LR table, partial norms,
+ *     coefficients, status, NCCL communicator) and frees it in lars_destroy.
+ *   * Argument errors are returned synchronously before anything is enqueued. Steps never synchronize
+ *     the host: numeric overflow is reported through lars_last_step_skipped, not a return code.
+ *   * `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   * One handle is driven by one host thread at a time, one in-flight step per handle.
+ */
+#ifndef LARS_B200_H
+#define LARS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LARS_OK = 0,
+  LARS_ERR_INVALID_ARG = 1, /* null pointer, bad hyper-parameter, bad rank                         */
+  LARS_ERR_LAYOUT = 2,      /* numel <= 0, unknown kind, n <= 0, layout hash differs across ranks   */
+  LARS_ERR_ITER_RANGE = 3,  /* iter outside [0, T)                                     */
+  LARS_ERR_ALIGNMENT = 4,   /* a base pointer is not 256-byte aligned                               */
+  LARS_ERR_CUDA = 5,        /* a CUDA runtime call failed                                           */
+  LARS_ERR_NCCL = 6,        /* an NCCL call failed                                                  */
+  LARS_ERR_OOM = 7,         /* device or host allocation failed                                     */
+  LARS_ERR_NO_COMM = 8,     /* dp step before lars_comm_init, or comm init on a P=1 handle          */
+  LARS_ERR_NO_DEVICE = 9    /* a device operation on a host-only (device = -1) handle               */
+} lars_status_t;
+
+/* Per-tensor kind (SPEC.md:33-36 ParamSegment.kind; reading #4). */
+typedef enum {
+  LARS_KIND_WEIGHT = 0,   /* conv / fc weights: LARS trust ratio + weight decay */
+  LARS_KIND_BIAS = 1,     /* skip kinds: lambda = 1, no weight decay            */
+  LARS_KIND_BN_GAMMA = 2,
+  LARS_KIND_BN_BETA = 3
+} lars_kind_t;
+
+/* Gradient wire dtype: fp16 is the paper's; bf16 optional; fp32 allowed. */
+typedef enum { LARS_F32 = 0, LARS_F16 = 1, LARS_BF16 = 2 } lars_dtype_t;
+
+typedef struct {
+  int64_t numel; /* > 0 */
+  int32_t kind;  /* lars_kind_t */
+  int32_t reserved;
+} lars_tensor_t;
+
+typedef struct {
+  double base_lr;        /* REQUIRED, > 0: the paper gives no value (reading #9)                 */
+  double eta;            /* LARS trust coefficient (default 1e-3, reading #5/#10)                 */
+  double momentum;       /* mu in [0, 1) (default 0.9)                                            */
+  double weight_decay;   /* beta >= 0, weight-kind tensors only (default 5e-5)                    */
+  double eps;            /* trust-ratio denominator guard >= 0 (default 0)                        */
+  double warmup_epochs;  /* W = round-half-up(warmup_epochs * ipe) iterations (default 5)         */
+  double poly_power;     /* p >= 0 (p = 1 linear, p = 0 constant; default 2)                       */
+  double grad_scale;     /* s: G = s * sum_r g_r (default 1.0; e.g. 1/(P*loss_scale))             */
+  int64_t global_batch;  /* B > 0 (default 81,920)                                    */
+  int64_t dataset_size;  /* D > 0 images per epoch (default 1,280,000)               */
+  int32_t total_epochs;  /* E > 0 (default 90)                                   */
+  int32_t grad_dtype;    /* lars_dtype_t of g                                                     */
+  int32_t nranks;        /* data-parallel world size P the layout is planned for (default 1)       */
+  int32_t tile_elems;    /* minimum work-tile size in elements; 0 = library default                */
+} lars_hparams_t;
+
+typedef struct lars_ctx* lars_handle_t;
+
+/* Fills *hp with the defaults listed above (base_lr = 0: the caller must set it). */
+void lars_hparams_default(lars_hparams_t* hp);
+
+/* Plans the flat layout (offsets, per-rank shards for hp->nranks, work tiles), the schedule
+ * (ipe = ceil(D/B), T = E*ipe, W) and the LR table lr[0..T) in double; uploads them to `device`.
+ * device = -1 builds a host-only handle (plan + schedule queries only; no CUDA calls).
+ * Errors: LARS_ERR_LAYOUT (n <= 0, numel <= 0, unknown kind), LARS_ERR_INVALID_ARG (bad hp),
+ * LARS_ERR_CUDA / LARS_ERR_OOM. No kernel runs. */
+lars_status_t lars_init(const lars_tensor_t* tensors, int32_t n, const lars_hparams_t* hp,
+                        int32_t device, lars_handle_t* out);
+
+/* offsets[n] (elements) of every tensor in the flat buffers, and the flat length. At P > 1 the
+ * layout is rank-major: rank r owns [r*S, (r+1)*S) (lars_shard_range) and holds whole tensors
+ * assigned by longest-processing-time bin packing. Either output may be NULL. */
+lars_status_t lars_layout(lars_handle_t h, int64_t* offsets, int64_t* padded_numel);
+
+/* Schedule: iterations per epoch, total iterations T, warm-up iterations W. Any output may be NULL. */
+lars_status_t lars_schedule(lars_handle_t h, int64_t* ipe, int64_t* total_iters, int64_t* warmup_iters);
+
+/* lr(iter) exactly as the kernels use it (double). LARS_ERR_ITER_RANGE outside [0, T). */
+lars_status_t lars_lr_at(lars_handle_t h, int64_t iter, double* lr);
+
+/* Element range [begin, end) of rank `rank`'s shard (P = 1: the whole flat buffer). */
+lars_status_t lars_shard_range(lars_handle_t h, int32_t rank, int64_t* begin, int64_t* end);
+
+/* owner[n]: the rank that updates each tensor. */
+lars_status_t lars_tensor_owner(lars_handle_t h, int32_t* owner);
+
+/* 64-bit FNV-1a hash of (layout, hyper-parameters, P); equal on every rank that planned alike. */
+lars_status_t lars_layout_hash(lars_handle_t h, uint64_t* hash);
+
+/* One LARS update of every tensor on one GPU: g is the already-combined gradient (P = 1 semantics,
+ * G = s*g). Enqueues the segmented norm kernel (K1: all per-layer ||w||, ||g||, lambda, lr*lambda,
+ * non-finite check) and the fused update kernel (K2: unscale + weight decay + momentum + update,
+ * streaming w, g, m once) on `stream`; returns without synchronizing. */
+lars_status_t lars_step(lars_handle_t h, float* w, const void* g, float* m, int64_t iter, void* stream);
+
+/* Same as lars_step, but the gradient comes from HOST memory g_host (pinned for async copies,
+ * padded_numel elements of grad_dtype): the library copies it into its own device staging buffer on
+ * `stream`, runs the step, and copies the step status + per-layer norms back into library-owned
+ * pinned memory (read them with lars_last_step_skipped / lars_last_norms). */
+lars_status_t lars_step_host_grad(lars_handle_t h, float* w, const void* g_host, float* m,
+                                  int64_t iter, void* stream);
+
+/* 128-byte NCCL unique id for lars_comm_init (rank 0 creates it; the caller broadcasts it). */
+lars_status_t lars_get_unique_id(void* id128);
+
+/* Creates the NCCL communicator for this handle (nranks must equal hp.nranks > 1), checks that every
+ * rank planned the same layout (hash min == max over ranks, else LARS_ERR_LAYOUT), and allocates the
+ * reduced-gradient shard buffer. Collective: every rank must call it. */
+lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, const void* id128);
+
+/* Data-parallel step on rank `rank` (P = hp.nranks):
+ *   C1 reduce-scatter:  gsum = sum_r g_r over the rank's shard (NCCL, wire dtype, NVLink)
+ *   K1 + K2 on the rank's shard only (m is shard-owned: only [begin, end) is read and written)
+ *   C2 all-gather:      every rank receives all updated fp32 weights (in place in w)
+ * g (the rank's local full gradient) is NOT modified. On completion (stream-ordered) w is bitwise
+ * identical on all ranks. Collective: every rank must call it with the same iter. */
+lars_status_t dp_allreduce_lars_step(lars_handle_t h, float* w, const void* g, float* m, int64_t iter,
+                                     void* stream);
+
+/* Same as dp_allreduce_lars_step with the rank's local gradient in HOST memory g_host (pinned for async
+ * copies, padded_numel elements): H2D copy into a library staging buffer, the dp step, then a D2H copy of
+ * the step status + per-layer norms into library-owned pinned memory, all on `stream`. */
+lars_status_t dp_allreduce_lars_step_host_grad(lars_handle_t h, float* w, const void* g_host, float* m,
+                                               int64_t iter, void* stream);
+
+/* Per-phase device timing with CUDA events recorded on the step's stream (instrumentation for benchmarks;
+ * off by default). lars_profile_enable(h, 1) clears the accumulators and starts recording;
+ * lars_profile_enable(h, 0) stops. lars_profile_read synchronizes and returns accumulated milliseconds per
+ * phase since enable: ms[0] reduce-scatter (C1), ms[1] norms (K1), ms[2] skip-flag allreduce (C3),
+ * ms[3] update (K2), ms[4] all-gather (C2); single-GPU steps fill ms[1] and ms[3]. *steps = steps timed. */
+lars_status_t lars_profile_enable(lars_handle_t h, int32_t enable);
+lars_status_t lars_profile_read(lars_handle_t h, double* ms, int64_t* steps);
+
+/* Device pointer to the reduced gradient shard of the last dp step (S elements of grad_dtype, first
+ * element = global element `begin` of this rank's shard). Owned by the library. */
+lars_status_t lars_reduced_grad(lars_handle_t h, const void** dev_ptr, int64_t* begin, int64_t* end);
+
+/* Synchronizing readbacks of the last step (per tensor; entries of tensors this rank does not own are
+ * left untouched). w_norm = ||w_l||, g_norm = ||G_l|| (grad_scale applied), lambda = trust ratio,
+ * coef = lr*lambda as the update kernel used it. Any output may be NULL. */
+lars_status_t lars_last_norms(lars_handle_t h, double* w_norm, double* g_norm, double* lambda, double* coef);
+lars_status_t lars_last_step_skipped(lars_handle_t h, int32_t* skipped);
+
+lars_status_t lars_destroy(lars_handle_t h);
+const char* lars_strerror(lars_status_t s);
+const char* lars_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LARS_B200_H */

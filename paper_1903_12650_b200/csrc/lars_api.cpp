@@ -1,0 +1,526 @@
+// C ABI implementation (include/lars.h): handle, device scratch, step issue, NCCL data-parallel path.
+//
+// Data-parallel step:
+//   C1  ncclReduceScatter(g -> gred, S, wire dtype, sum)       "gradients ... combined" PAPER.md:31;
+//                                                             fp16 on the wire PAPER.md:183;
+//                                                             one multi-MB message PAPER.md:147-153
+//   K1  per-layer norms + trust ratio on the rank's shard
+//   C3  ncclAllReduce(skip flag, max)                           whole-step skip is global (reading #13)
+//   K2  fused update of the shard
+//   C2  ncclAllGather(w shard -> w)                             every replica holds the owner's fp32 weights
+// Everything is stream-ordered: no host synchronization inside a step (CUDA-graph capturable).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <array>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "internal.h"
+
+using namespace lars;
+
+namespace {
+
+struct DevBufs {
+  WorkList wl;
+  DevWork dw{};
+  DevScratch sc{};
+  void* mem = nullptr;
+};
+
+size_t dtype_size(int32_t dt) { return dt == LARS_F32 ? 4 : 2; }
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+template <typename T>
+T* carve(char*& p, size_t n) {
+  T* r = reinterpret_cast<T*>(p);
+  p += (n * sizeof(T) + 255) / 256 * 256;
+  return r;
+}
+
+lars_status_t upload(DevBufs& b) {
+  const WorkList& wl = b.wl;
+  const size_t ns = std::max<size_t>(wl.segs.size(), 1), nt = std::max<size_t>(wl.tensors.size(), 1),
+               ntl = wl.tile_seg.size();
+  size_t bytes = 0;
+  auto add = [&](size_t n, size_t sz) { bytes += (n * sz + 255) / 256 * 256; };
+  add(ns, sizeof(Seg)); add(ntl, 4); add(nt, 4); add(nt, 4); add(nt, 4);                // work list
+  add(ns, 8); add(ns, 8); add(nt, 4); add(1, 4); add(1, 4); add(1, 4);                  // partials, counters
+  add(nt, 8); add(nt, 8); add(nt, 8); add(nt, 4); add(nt, 4);                           // outputs
+  if (cudaMalloc(&b.mem, bytes) != cudaSuccess) return LARS_ERR_OOM;
+  if (cudaMemset(b.mem, 0, bytes) != cudaSuccess) return LARS_ERR_CUDA;
+  char* p = (char*)b.mem;
+  Seg* segs = carve<Seg>(p, ns);
+  int32_t* tile_seg = carve<int32_t>(p, ntl);
+  int32_t* tsb = carve<int32_t>(p, nt);
+  int32_t* tsc = carve<int32_t>(p, nt);
+  int32_t* tl = carve<int32_t>(p, nt);
+  b.sc.part_w = carve<double>(p, ns);
+  b.sc.part_g = carve<double>(p, ns);
+  b.sc.seg_done = carve<unsigned>(p, nt);
+  b.sc.tensors_done = carve<unsigned>(p, 1);
+  b.sc.nonfinite = carve<unsigned>(p, 1);
+  b.sc.skip = carve<int32_t>(p, 1);
+  b.sc.w_norm = carve<double>(p, nt);
+  b.sc.g_norm = carve<double>(p, nt);
+  b.sc.lambda = carve<double>(p, nt);
+  b.sc.coef = carve<float>(p, nt);
+  b.sc.beta = carve<float>(p, nt);
+  auto cp = [](void* d, const void* s, size_t n) { return n == 0 || cudaMemcpy(d, s, n, cudaMemcpyHostToDevice) == cudaSuccess; };
+  if (!(cp(segs, wl.segs.data(), wl.segs.size() * sizeof(Seg)) && cp(tile_seg, wl.tile_seg.data(), ntl * 4) &&
+        cp(tsb, wl.tseg_begin.data(), wl.tseg_begin.size() * 4) &&
+        cp(tsc, wl.tseg_count.data(), wl.tseg_count.size() * 4) && cp(tl, wl.tlars.data(), wl.tlars.size() * 4)))
+    return LARS_ERR_CUDA;
+  b.dw = DevWork{segs, tile_seg, tsb, tsc, tl, wl.ntiles(), (int32_t)wl.tensors.size()};
+  return LARS_OK;
+}
+
+}  // namespace
+
+// Optional per-phase event timing (lars_profile_*): one set of 6 events per profiled step.
+struct Profiler {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::array<cudaEvent_t, 6>> pending;
+  std::vector<int> pending_kind;  // 1 = single GPU, 2 = data parallel
+  double acc[5] = {0, 0, 0, 0, 0};
+  int64_t steps = 0;
+  cudaEvent_t get() {
+    cudaEvent_t e = nullptr;
+    if (!pool.empty()) { e = pool.back(); pool.pop_back(); return e; }
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    return e;
+  }
+  std::array<cudaEvent_t, 6>* begin(int kind) {
+    if (!on) return nullptr;
+    std::array<cudaEvent_t, 6> s;
+    for (auto& e : s) e = get();
+    pending.push_back(s);
+    pending_kind.push_back(kind);
+    return &pending.back();
+  }
+};
+
+static void prof_rec(std::array<cudaEvent_t, 6>* p, int i, cudaStream_t s) {
+  if (p && (*p)[i]) cudaEventRecord((*p)[i], s);
+}
+
+struct lars_ctx {
+  Plan plan;
+  lars_hparams_t hp{};
+  int device = -1;
+  int sms = 148;
+  double* lr_d = nullptr;
+  DevBufs full, shard;
+  bool shard_ready = false;
+  ncclComm_t comm = nullptr;
+  int rank = 0;
+  void* gred = nullptr;
+  void* gstage = nullptr;
+  void* pinned = nullptr;  // host mirror of skip + norms for lars_step_host_grad
+  cudaStream_t last_stream = nullptr;
+  const DevBufs* last = nullptr;
+  Profiler prof;
+};
+
+#define CUDA_OR(expr)                                      \
+  do {                                                     \
+    if ((expr) != cudaSuccess) return LARS_ERR_CUDA;       \
+  } while (0)
+#define NCCL_OR(expr)                                      \
+  do {                                                     \
+    if ((expr) != ncclSuccess) return LARS_ERR_NCCL;       \
+  } while (0)
+
+static bool aligned256(const void* p) { return ((uintptr_t)p & 255u) == 0; }
+static ncclDataType_t nccl_type(int32_t dt) {
+  return dt == LARS_F32 ? ncclFloat32 : dt == LARS_F16 ? ncclFloat16 : ncclBfloat16;
+}
+
+extern "C" {
+
+void lars_hparams_default(lars_hparams_t* hp) {
+  if (!hp) return;
+  std::memset(hp, 0, sizeof *hp);
+  hp->base_lr = 0.0;
+  hp->eta = 1e-3;
+  hp->momentum = 0.9;
+  hp->weight_decay = 5e-5;
+  hp->eps = 0.0;
+  hp->warmup_epochs = 5.0;
+  hp->poly_power = 2.0;
+  hp->grad_scale = 1.0;
+  hp->global_batch = 81920;
+  hp->dataset_size = 1280000;
+  hp->total_epochs = 90;
+  hp->grad_dtype = LARS_F16;
+  hp->nranks = 1;
+  hp->tile_elems = 0;
+}
+
+const char* lars_version(void) { return "lars-b200 0.1 (sm_100a)"; }
+
+const char* lars_strerror(lars_status_t s) {
+  switch (s) {
+    case LARS_OK: return "ok";
+    case LARS_ERR_INVALID_ARG: return "invalid argument";
+    case LARS_ERR_LAYOUT: return "invalid layout (or layout differs across ranks)";
+    case LARS_ERR_ITER_RANGE: return "iteration outside [0, T)";
+    case LARS_ERR_ALIGNMENT: return "buffer not 256-byte aligned";
+    case LARS_ERR_CUDA: return "CUDA error";
+    case LARS_ERR_NCCL: return "NCCL error";
+    case LARS_ERR_OOM: return "out of memory";
+    case LARS_ERR_NO_COMM: return "no communicator (call lars_comm_init on a handle planned for nranks > 1)";
+    case LARS_ERR_NO_DEVICE: return "host-only handle (device = -1)";
+  }
+  return "unknown status";
+}
+
+lars_status_t lars_init(const lars_tensor_t* tensors, int32_t n, const lars_hparams_t* hp, int32_t device,
+                        lars_handle_t* out) {
+  if (!out || !hp) return LARS_ERR_INVALID_ARG;
+  *out = nullptr;
+  lars_ctx* h = new (std::nothrow) lars_ctx();
+  if (!h) return LARS_ERR_OOM;
+  lars_status_t st = make_plan(tensors, n, *hp, h->plan);
+  if (st != LARS_OK) { delete h; return st; }
+  h->hp = *hp;
+  h->device = device;
+  const int32_t min_tile = hp->tile_elems > 0 ? hp->tile_elems : kDefaultMinTile;
+  if (device >= 0) {
+    DeviceGuard g(device);
+    if (!g.ok) { delete h; return LARS_ERR_CUDA; }
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0) h->sms = sms;
+  }
+  h->full.wl = make_worklist(h->plan, -1, h->sms * kCtasPerSm, min_tile);
+  if (device >= 0) {
+    DeviceGuard g(device);
+    if (cudaMalloc(&h->lr_d, h->plan.lr.size() * sizeof(double)) != cudaSuccess) { lars_destroy(h); return LARS_ERR_OOM; }
+    if (cudaMemcpy(h->lr_d, h->plan.lr.data(), h->plan.lr.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) {
+      lars_destroy(h);
+      return LARS_ERR_CUDA;
+    }
+    st = upload(h->full);
+    if (st != LARS_OK) { lars_destroy(h); return st; }
+  }
+  *out = h;
+  return LARS_OK;
+}
+
+lars_status_t lars_layout(lars_handle_t h, int64_t* offsets, int64_t* padded_numel) {
+  if (!h) return LARS_ERR_INVALID_ARG;
+  if (offsets) std::copy(h->plan.offset.begin(), h->plan.offset.end(), offsets);
+  if (padded_numel) *padded_numel = h->plan.padded;
+  return LARS_OK;
+}
+
+lars_status_t lars_schedule(lars_handle_t h, int64_t* ipe, int64_t* total_iters, int64_t* warmup_iters) {
+  if (!h) return LARS_ERR_INVALID_ARG;
+  if (ipe) *ipe = h->plan.ipe;
+  if (total_iters) *total_iters = h->plan.T;
+  if (warmup_iters) *warmup_iters = h->plan.W;
+  return LARS_OK;
+}
+
+lars_status_t lars_lr_at(lars_handle_t h, int64_t iter, double* lr) {
+  if (!h || !lr) return LARS_ERR_INVALID_ARG;
+  if (iter < 0 || iter >= h->plan.T) return LARS_ERR_ITER_RANGE;
+  *lr = h->plan.lr[iter];
+  return LARS_OK;
+}
+
+lars_status_t lars_shard_range(lars_handle_t h, int32_t rank, int64_t* begin, int64_t* end) {
+  if (!h || rank < 0 || rank >= h->plan.P) return LARS_ERR_INVALID_ARG;
+  if (begin) *begin = (int64_t)rank * h->plan.S;
+  if (end) *end = (int64_t)(rank + 1) * h->plan.S;
+  return LARS_OK;
+}
+
+lars_status_t lars_tensor_owner(lars_handle_t h, int32_t* owner) {
+  if (!h || !owner) return LARS_ERR_INVALID_ARG;
+  std::copy(h->plan.owner.begin(), h->plan.owner.end(), owner);
+  return LARS_OK;
+}
+
+lars_status_t lars_layout_hash(lars_handle_t h, uint64_t* hash) {
+  if (!h || !hash) return LARS_ERR_INVALID_ARG;
+  *hash = h->plan.hash;
+  return LARS_OK;
+}
+
+static lars_status_t check_step_args(lars_handle_t h, const void* w, const void* g, const void* m, int64_t iter) {
+  if (!h || !w || !g || !m) return LARS_ERR_INVALID_ARG;
+  if (h->device < 0) return LARS_ERR_NO_DEVICE;
+  if (iter < 0 || iter >= h->plan.T) return LARS_ERR_ITER_RANGE;
+  if (!aligned256(w) || !aligned256(g) || !aligned256(m)) return LARS_ERR_ALIGNMENT;
+  return LARS_OK;
+}
+
+static Hyper hyper(lars_handle_t h, int64_t iter) {
+  return Hyper{h->lr_d, iter, h->hp.eta, h->hp.weight_decay, h->hp.eps, h->hp.grad_scale,
+               (float)h->hp.momentum, (float)h->hp.grad_scale};
+}
+
+lars_status_t lars_step(lars_handle_t h, float* w, const void* g, float* m, int64_t iter, void* stream) {
+  lars_status_t st = check_step_args(h, w, g, m, iter);
+  if (st != LARS_OK) return st;
+  DeviceGuard dg(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const Hyper hy = hyper(h, iter);
+  auto* pe = h->prof.begin(1);
+  prof_rec(pe, 0, s);
+  CUDA_OR(launch_norms(h->hp.grad_dtype, h->full.dw, h->full.sc, hy, w, g, 0, s));       // K1
+  prof_rec(pe, 1, s);
+  CUDA_OR(launch_update(h->hp.grad_dtype, h->full.dw, h->full.sc, hy, w, g, 0, m, s));   // K2
+  prof_rec(pe, 2, s);
+  h->last_stream = s;
+  h->last = &h->full;
+  return LARS_OK;
+}
+
+static lars_status_t stage_host_grad(lars_handle_t h, const void* g_host, cudaStream_t s);
+static lars_status_t readback_status(lars_handle_t h, const DevBufs& b, cudaStream_t s);
+
+lars_status_t lars_step_host_grad(lars_handle_t h, float* w, const void* g_host, float* m, int64_t iter,
+                                  void* stream) {
+  if (!h || !g_host) return LARS_ERR_INVALID_ARG;
+  if (h->device < 0) return LARS_ERR_NO_DEVICE;
+  DeviceGuard dg(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  lars_status_t st = stage_host_grad(h, g_host, s);
+  if (st != LARS_OK) return st;
+  st = lars_step(h, w, h->gstage, m, iter, stream);
+  if (st != LARS_OK) return st;
+  return readback_status(h, h->full, s);
+}
+
+lars_status_t lars_get_unique_id(void* id128) {
+  if (!id128) return LARS_ERR_INVALID_ARG;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  NCCL_OR(ncclGetUniqueId(reinterpret_cast<ncclUniqueId*>(id128)));
+  return LARS_OK;
+}
+
+lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, const void* id128) {
+  if (!h || !id128) return LARS_ERR_INVALID_ARG;
+  if (h->device < 0) return LARS_ERR_NO_DEVICE;
+  if (h->plan.P <= 1) return LARS_ERR_NO_COMM;
+  if (nranks != h->plan.P || rank < 0 || rank >= nranks) return LARS_ERR_INVALID_ARG;
+  if (h->comm) return LARS_ERR_INVALID_ARG;
+  DeviceGuard dg(h->device);
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof id);
+  NCCL_OR(ncclCommInitRank(&h->comm, nranks, id, rank));
+  h->rank = rank;
+  // Layout agreement (static plan): min and max of the hash over ranks must match.
+  uint64_t* d = nullptr;
+  CUDA_OR(cudaMalloc(&d, 2 * sizeof(uint64_t)));
+  const uint64_t hv[2] = {h->plan.hash, h->plan.hash};
+  cudaStream_t s;
+  CUDA_OR(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  CUDA_OR(cudaMemcpyAsync(d, hv, sizeof hv, cudaMemcpyHostToDevice, s));
+  NCCL_OR(ncclGroupStart());
+  NCCL_OR(ncclAllReduce(d, d, 1, ncclUint64, ncclMin, h->comm, s));
+  NCCL_OR(ncclAllReduce(d + 1, d + 1, 1, ncclUint64, ncclMax, h->comm, s));
+  NCCL_OR(ncclGroupEnd());
+  uint64_t r[2] = {0, 0};
+  CUDA_OR(cudaMemcpyAsync(r, d, sizeof r, cudaMemcpyDeviceToHost, s));
+  CUDA_OR(cudaStreamSynchronize(s));
+  cudaStreamDestroy(s);
+  cudaFree(d);
+  if (r[0] != h->plan.hash || r[1] != h->plan.hash) return LARS_ERR_LAYOUT;
+  const int32_t min_tile = h->hp.tile_elems > 0 ? h->hp.tile_elems : kDefaultMinTile;
+  h->shard.wl = make_worklist(h->plan, rank, h->sms * kCtasPerSm, min_tile);
+  lars_status_t st = upload(h->shard);
+  if (st != LARS_OK) return st;
+  if (cudaMalloc(&h->gred, (size_t)h->plan.S * dtype_size(h->hp.grad_dtype)) != cudaSuccess) return LARS_ERR_OOM;
+  CUDA_OR(cudaMemset(h->gred, 0, (size_t)h->plan.S * dtype_size(h->hp.grad_dtype)));
+  h->shard_ready = true;
+  return LARS_OK;
+}
+
+lars_status_t dp_allreduce_lars_step(lars_handle_t h, float* w, const void* g, float* m, int64_t iter,
+                                     void* stream) {
+  lars_status_t st = check_step_args(h, w, g, m, iter);
+  if (st != LARS_OK) return st;
+  if (!h->comm || !h->shard_ready) return LARS_ERR_NO_COMM;
+  DeviceGuard dg(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t S = h->plan.S, begin = (int64_t)h->rank * S;
+  const int32_t dt = h->hp.grad_dtype;
+  const Hyper hy = hyper(h, iter);
+  auto* pe = h->prof.begin(2);
+  prof_rec(pe, 0, s);
+  NCCL_OR(ncclReduceScatter(g, h->gred, (size_t)S, nccl_type(dt), ncclSum, h->comm, s));          // C1
+  prof_rec(pe, 1, s);
+  CUDA_OR(launch_norms(dt, h->shard.dw, h->shard.sc, hy, w, h->gred, begin, s));                   // K1
+  prof_rec(pe, 2, s);
+  NCCL_OR(ncclAllReduce(h->shard.sc.skip, h->shard.sc.skip, 1, ncclInt32, ncclMax, h->comm, s));  // C3
+  prof_rec(pe, 3, s);
+  CUDA_OR(launch_update(dt, h->shard.dw, h->shard.sc, hy, w, h->gred, begin, m, s));               // K2
+  prof_rec(pe, 4, s);
+  NCCL_OR(ncclAllGather(w + begin, w, (size_t)S, ncclFloat32, h->comm, s));                       // C2
+  prof_rec(pe, 5, s);
+  h->last_stream = s;
+  h->last = &h->shard;
+  return LARS_OK;
+}
+
+static lars_status_t stage_host_grad(lars_handle_t h, const void* g_host, cudaStream_t s) {
+  const size_t gbytes = (size_t)h->plan.padded * dtype_size(h->hp.grad_dtype);
+  const size_t L = (size_t)h->plan.L;
+  if (!h->gstage) {
+    if (cudaMalloc(&h->gstage, gbytes) != cudaSuccess) { h->gstage = nullptr; return LARS_ERR_OOM; }
+    if (cudaMallocHost(&h->pinned, 256 + 2 * L * sizeof(double)) != cudaSuccess) { h->pinned = nullptr; return LARS_ERR_OOM; }
+  }
+  CUDA_OR(cudaMemcpyAsync(h->gstage, g_host, gbytes, cudaMemcpyHostToDevice, s));
+  return LARS_OK;
+}
+
+static lars_status_t readback_status(lars_handle_t h, const DevBufs& b, cudaStream_t s) {
+  char* pin = (char*)h->pinned;
+  const size_t nt = b.wl.tensors.size();
+  CUDA_OR(cudaMemcpyAsync(pin, b.sc.skip, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  if (nt) {
+    CUDA_OR(cudaMemcpyAsync(pin + 256, b.sc.w_norm, nt * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CUDA_OR(cudaMemcpyAsync(pin + 256 + nt * sizeof(double), b.sc.g_norm, nt * sizeof(double), cudaMemcpyDeviceToHost, s));
+  }
+  return LARS_OK;
+}
+
+lars_status_t dp_allreduce_lars_step_host_grad(lars_handle_t h, float* w, const void* g_host, float* m, int64_t iter,
+                                               void* stream) {
+  if (!h || !g_host) return LARS_ERR_INVALID_ARG;
+  if (h->device < 0) return LARS_ERR_NO_DEVICE;
+  if (!h->comm || !h->shard_ready) return LARS_ERR_NO_COMM;
+  DeviceGuard dg(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  lars_status_t st = stage_host_grad(h, g_host, s);
+  if (st != LARS_OK) return st;
+  st = dp_allreduce_lars_step(h, w, h->gstage, m, iter, stream);
+  if (st != LARS_OK) return st;
+  return readback_status(h, h->shard, s);
+}
+
+lars_status_t lars_profile_enable(lars_handle_t h, int32_t enable) {
+  if (!h) return LARS_ERR_INVALID_ARG;
+  if (h->device < 0) return LARS_ERR_NO_DEVICE;
+  DeviceGuard dg(h->device);
+  for (auto& s : h->prof.pending)
+    for (auto e : s)
+      if (e) h->prof.pool.push_back(e);
+  h->prof.pending.clear();
+  h->prof.pending_kind.clear();
+  for (double& a : h->prof.acc) a = 0;
+  h->prof.steps = 0;
+  h->prof.on = enable != 0;
+  return LARS_OK;
+}
+
+lars_status_t lars_profile_read(lars_handle_t h, double* ms, int64_t* steps) {
+  if (!h) return LARS_ERR_INVALID_ARG;
+  if (h->device < 0) return LARS_ERR_NO_DEVICE;
+  DeviceGuard dg(h->device);
+  Profiler& p = h->prof;
+  for (size_t i = 0; i < p.pending.size(); ++i) {
+    auto& ev = p.pending[i];
+    const int last = p.pending_kind[i] == 1 ? 2 : 5;
+    CUDA_OR(cudaEventSynchronize(ev[last]));
+    float t = 0;
+    if (p.pending_kind[i] == 1) {
+      CUDA_OR(cudaEventElapsedTime(&t, ev[0], ev[1])); p.acc[1] += t;
+      CUDA_OR(cudaEventElapsedTime(&t, ev[1], ev[2])); p.acc[3] += t;
+    } else {
+      for (int k = 0; k < 5; ++k) { CUDA_OR(cudaEventElapsedTime(&t, ev[k], ev[k + 1])); p.acc[k] += t; }
+    }
+    for (auto e : ev) p.pool.push_back(e);
+    ++p.steps;
+  }
+  p.pending.clear();
+  p.pending_kind.clear();
+  if (ms) std::copy(p.acc, p.acc + 5, ms);
+  if (steps) *steps = p.steps;
+  return LARS_OK;
+}
+
+lars_status_t lars_reduced_grad(lars_handle_t h, const void** dev_ptr, int64_t* begin, int64_t* end) {
+  if (!h || !dev_ptr) return LARS_ERR_INVALID_ARG;
+  if (!h->gred) return LARS_ERR_NO_COMM;
+  *dev_ptr = h->gred;
+  if (begin) *begin = (int64_t)h->rank * h->plan.S;
+  if (end) *end = (int64_t)(h->rank + 1) * h->plan.S;
+  return LARS_OK;
+}
+
+lars_status_t lars_last_norms(lars_handle_t h, double* w_norm, double* g_norm, double* lambda, double* coef) {
+  if (!h) return LARS_ERR_INVALID_ARG;
+  if (h->device < 0) return LARS_ERR_NO_DEVICE;
+  const DevBufs* b = h->last ? h->last : &h->full;
+  DeviceGuard dg(h->device);
+  CUDA_OR(cudaStreamSynchronize(h->last_stream));
+  const size_t nt = b->wl.tensors.size();
+  std::vector<double> wn(nt), gn(nt), la(nt);
+  std::vector<float> cf(nt);
+  if (nt) {
+    CUDA_OR(cudaMemcpy(wn.data(), b->sc.w_norm, nt * 8, cudaMemcpyDeviceToHost));
+    CUDA_OR(cudaMemcpy(gn.data(), b->sc.g_norm, nt * 8, cudaMemcpyDeviceToHost));
+    CUDA_OR(cudaMemcpy(la.data(), b->sc.lambda, nt * 8, cudaMemcpyDeviceToHost));
+    CUDA_OR(cudaMemcpy(cf.data(), b->sc.coef, nt * 4, cudaMemcpyDeviceToHost));
+  }
+  for (size_t i = 0; i < nt; ++i) {
+    const int32_t l = b->wl.tensors[i];
+    if (w_norm) w_norm[l] = wn[i];
+    if (g_norm) g_norm[l] = gn[i];
+    if (lambda) lambda[l] = la[i];
+    if (coef) coef[l] = (double)cf[i];
+  }
+  return LARS_OK;
+}
+
+lars_status_t lars_last_step_skipped(lars_handle_t h, int32_t* skipped) {
+  if (!h || !skipped) return LARS_ERR_INVALID_ARG;
+  if (h->device < 0) return LARS_ERR_NO_DEVICE;
+  const DevBufs* b = h->last ? h->last : &h->full;
+  DeviceGuard dg(h->device);
+  CUDA_OR(cudaStreamSynchronize(h->last_stream));
+  CUDA_OR(cudaMemcpy(skipped, b->sc.skip, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  return LARS_OK;
+}
+
+lars_status_t lars_destroy(lars_handle_t h) {
+  if (!h) return LARS_ERR_INVALID_ARG;
+  if (h->device >= 0) {
+    DeviceGuard dg(h->device);
+    if (h->comm) ncclCommDestroy(h->comm);
+    cudaFree(h->lr_d);
+    cudaFree(h->full.mem);
+    cudaFree(h->shard.mem);
+    cudaFree(h->gred);
+    cudaFree(h->gstage);
+    if (h->pinned) cudaFreeHost(h->pinned);
+    for (auto& st : h->prof.pending)
+      for (auto e : st)
+        if (e) cudaEventDestroy(e);
+    for (auto e : h->prof.pool) cudaEventDestroy(e);
+  }
+  delete h;
+  return LARS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,179 @@
+// Host-side planner: flat layout, per-rank shards, work tiles, learning-rate schedule, layout hash.
+// Runs once in lars_init. Pure C++: works on a host-only (device = -1) handle.
+//
+//  * Static planning "beforehand" (§III-C-2): every rank computes the same plan
+//    from the same inputs with no communication; lars_comm_init only verifies the hash.
+//  * Schedule (PAPER.md:96-103 warm-up + decay; PAPER.md:210-211 16 updates/epoch, 1,440 total).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "internal.h"
+
+namespace lars {
+
+static int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+lars_status_t validate_hparams(const lars_hparams_t& hp) {
+  auto fin = [](double x) { return std::isfinite(x); };
+  if (!(fin(hp.base_lr) && hp.base_lr > 0)) return LARS_ERR_INVALID_ARG;
+  if (!(fin(hp.eta) && hp.eta >= 0)) return LARS_ERR_INVALID_ARG;
+  if (!(fin(hp.momentum) && hp.momentum >= 0 && hp.momentum < 1)) return LARS_ERR_INVALID_ARG;
+  if (!(fin(hp.weight_decay) && hp.weight_decay >= 0)) return LARS_ERR_INVALID_ARG;
+  if (!(fin(hp.eps) && hp.eps >= 0)) return LARS_ERR_INVALID_ARG;
+  if (!(fin(hp.warmup_epochs) && hp.warmup_epochs >= 0)) return LARS_ERR_INVALID_ARG;
+  if (!(fin(hp.poly_power) && hp.poly_power >= 0)) return LARS_ERR_INVALID_ARG;
+  if (!(fin(hp.grad_scale) && hp.grad_scale != 0)) return LARS_ERR_INVALID_ARG;
+  if (hp.global_batch <= 0 || hp.dataset_size <= 0 || hp.total_epochs <= 0) return LARS_ERR_INVALID_ARG;
+  if (hp.grad_dtype < LARS_F32 || hp.grad_dtype > LARS_BF16) return LARS_ERR_INVALID_ARG;
+  if (hp.nranks < 1 || hp.nranks > 4096) return LARS_ERR_INVALID_ARG;
+  if (hp.tile_elems < 0) return LARS_ERR_INVALID_ARG;
+  return LARS_OK;
+}
+
+// ---- schedule -------------------------------------------------------------------------------
+// ipe = ceil(D/B) (1,280,000/81,920 -> 16); T = E*ipe (1,440);
+// W = round-half-up(warmup_epochs*ipe) (reading #7).
+// lr(t) = base*(t+1)/W for t < W (linear warm-up, reading #6);
+// lr(t) = base*((T-t)/(T-W))^p for W <= t < T (polynomial decay, reading #8;
+//         (T-t)/(T-W) == 1-(t-W)/(T-W) without the cancellation near t = T-1).
+static lars_status_t make_schedule(const lars_hparams_t& hp, Plan& p) {
+  p.ipe = (hp.dataset_size + hp.global_batch - 1) / hp.global_batch;
+  p.T = (int64_t)hp.total_epochs * p.ipe;
+  p.W = (int64_t)std::floor(hp.warmup_epochs * (double)p.ipe + 0.5);
+  if (p.W > p.T || p.T > (int64_t)1 << 26) return LARS_ERR_INVALID_ARG;
+  p.lr.resize(p.T);
+  for (int64_t t = 0; t < p.T; ++t) {
+    if (t < p.W)
+      p.lr[t] = hp.base_lr * (double)(t + 1) / (double)p.W;
+    else
+      p.lr[t] = hp.base_lr * std::pow((double)(p.T - t) / (double)(p.T - p.W), hp.poly_power);
+  }
+  return LARS_OK;
+}
+
+// ---- layout ---------------------------------------------------------------------------------
+// P = 1: tensors in the given order, each at a 64-element aligned offset.
+// P > 1: whole-tensor longest-processing-time bin packing (ties: larger tensor first, then lower
+// index; equal loads -> lower rank), rank-major: rank r owns [r*S, (r+1)*S), tensors inside a shard
+// in index order. No tensor spans ranks, so every per-layer norm is local (SURVEY.md §8(e) "D1").
+static void make_layout(Plan& p) {
+  const int32_t L = p.L, P = p.P;
+  std::vector<int64_t> asz(L);
+  for (int32_t l = 0; l < L; ++l) asz[l] = round_up(p.numel[l], kAlign);
+  p.owner.assign(L, 0);
+  p.offset.assign(L, 0);
+  if (P == 1) {
+    int64_t off = 0;
+    for (int32_t l = 0; l < L; ++l) { p.offset[l] = off; off += asz[l]; }
+    p.S = p.padded = std::max<int64_t>(off, kAlign);
+    return;
+  }
+  std::vector<int32_t> order(L);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return asz[a] > asz[b]; });
+  std::vector<int64_t> load(P, 0);
+  for (int32_t l : order) {
+    int32_t best = 0;
+    for (int32_t r = 1; r < P; ++r)
+      if (load[r] < load[best]) best = r;
+    p.owner[l] = best;
+    load[best] += asz[l];
+  }
+  int64_t S = std::max<int64_t>(*std::max_element(load.begin(), load.end()), kAlign);
+  p.S = round_up(S, kAlign);
+  p.padded = p.S * P;
+  std::vector<int64_t> fill(P, 0);
+  for (int32_t l = 0; l < L; ++l) {
+    int32_t r = p.owner[l];
+    p.offset[l] = (int64_t)r * p.S + fill[r];
+    fill[r] += asz[l];
+  }
+}
+
+static uint64_t fnv1a(uint64_t h, const void* data, size_t n) {
+  const unsigned char* c = (const unsigned char*)data;
+  for (size_t i = 0; i < n; ++i) { h ^= c[i]; h *= 1099511628211ull; }
+  return h;
+}
+
+lars_status_t make_plan(const lars_tensor_t* t, int32_t n, const lars_hparams_t& hp, Plan& p) {
+  if (n <= 0 || t == nullptr) return LARS_ERR_LAYOUT;
+  lars_status_t st = validate_hparams(hp);
+  if (st != LARS_OK) return st;
+  p.L = n;
+  p.P = hp.nranks;
+  p.numel.resize(n);
+  p.kind.resize(n);
+  for (int32_t l = 0; l < n; ++l) {
+    if (t[l].numel <= 0 || t[l].numel > ((int64_t)1 << 40)) return LARS_ERR_LAYOUT;
+    if (t[l].kind < LARS_KIND_WEIGHT || t[l].kind > LARS_KIND_BN_BETA) return LARS_ERR_LAYOUT;
+    p.numel[l] = t[l].numel;
+    p.kind[l] = t[l].kind;
+  }
+  st = make_schedule(hp, p);
+  if (st != LARS_OK) return st;
+  make_layout(p);
+  uint64_t h = 1469598103934665603ull;
+  h = fnv1a(h, &p.L, sizeof p.L);
+  h = fnv1a(h, &p.P, sizeof p.P);
+  h = fnv1a(h, p.numel.data(), p.numel.size() * sizeof(int64_t));
+  h = fnv1a(h, p.kind.data(), p.kind.size() * sizeof(int32_t));
+  h = fnv1a(h, p.offset.data(), p.offset.size() * sizeof(int64_t));
+  const double hd[] = {hp.base_lr, hp.eta, hp.momentum, hp.weight_decay, hp.eps, hp.warmup_epochs,
+                       hp.poly_power, hp.grad_scale};
+  h = fnv1a(h, hd, sizeof hd);
+  const int64_t hi[] = {hp.global_batch, hp.dataset_size, hp.total_epochs, hp.grad_dtype};
+  h = fnv1a(h, hi, sizeof hi);
+  p.hash = h;
+  return LARS_OK;
+}
+
+// ---- work tiles -----------------------------------------------------------------------------
+// The tensors of the work set are walked in flat order and cut into tiles of ~E/ntiles elements
+// (E = elements of the work set, at least min_tile, a multiple of 64). Cuts inside a tensor fall on
+// 64-element boundaries, so every segment starts 256-byte aligned for fp32. Every CTA then streams
+// the same number of bytes whatever the tensor-size mix (most ResNet-50 layers are
+// too small to occupy a GPU on their own).
+WorkList make_worklist(const Plan& p, int32_t rank, int32_t ntiles_target, int32_t min_tile) {
+  WorkList wl;
+  std::vector<int32_t> ids;
+  for (int32_t l = 0; l < p.L; ++l)
+    if (rank < 0 || p.owner[l] == rank) ids.push_back(l);
+  std::stable_sort(ids.begin(), ids.end(), [&](int32_t a, int32_t b) { return p.offset[a] < p.offset[b]; });
+  for (int32_t l : ids) wl.elems += p.numel[l];
+  int64_t target = std::max<int64_t>(min_tile, (wl.elems + ntiles_target - 1) / std::max(1, ntiles_target));
+  target = std::min<int64_t>(round_up(target, kAlign), (int64_t)1 << 30);
+  wl.tile_seg.push_back(0);
+  int64_t fill = 0;
+  for (size_t li = 0; li < ids.size(); ++li) {
+    const int32_t l = ids[li];
+    wl.tensors.push_back(l);
+    wl.tlars.push_back(p.kind[l] == LARS_KIND_WEIGHT ? 1 : 0);
+    wl.tseg_begin.push_back((int32_t)wl.segs.size());
+    int64_t pos = 0;
+    while (pos < p.numel[l]) {
+      int64_t room = target - fill;
+      int64_t take = std::min<int64_t>(p.numel[l] - pos, room);
+      if (take < p.numel[l] - pos) take = take / kAlign * kAlign;  // interior cut: 64-aligned
+      if (take <= 0) {  // tile full
+        wl.tile_seg.push_back((int32_t)wl.segs.size());
+        fill = 0;
+        continue;
+      }
+      wl.segs.push_back(Seg{p.offset[l] + pos, (int32_t)take, (int32_t)li});
+      pos += take;
+      fill += take;
+      if (fill >= target) {
+        wl.tile_seg.push_back((int32_t)wl.segs.size());
+        fill = 0;
+      }
+    }
+    wl.tseg_count.push_back((int32_t)wl.segs.size() - wl.tseg_begin.back());
+  }
+  if (fill > 0 || wl.tile_seg.size() == 1) wl.tile_seg.push_back((int32_t)wl.segs.size());
+  return wl;
+}
+
+}  // namespace lars
