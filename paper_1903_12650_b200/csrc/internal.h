@@ -13,8 +13,23 @@ namespace lars {
 
 constexpr int64_t kAlign = 64;          // element alignment of every tensor (256 B of fp32)
 constexpr int kThreads = 256;           // threads per CTA of K1 / K2
-constexpr int kCtasPerSm = 2;           // resident CTAs per SM the tile plan targets
+#ifndef LARS_NORM_CTAS_PER_SM
+#define LARS_NORM_CTAS_PER_SM 4
+#endif
+#ifndef LARS_UPDATE_CTAS_PER_SM
+#define LARS_UPDATE_CTAS_PER_SM 4
+#endif
+#ifndef LARS_NORM_UNROLL
+#define LARS_NORM_UNROLL 2
+#endif
+constexpr int kCtasPerSm = LARS_NORM_CTAS_PER_SM;      // K1 resident CTAs per SM (one static tile each)
+constexpr int kUpdCtasPerSm = LARS_UPDATE_CTAS_PER_SM; // K2 resident CTAs per SM (dynamic items)
+constexpr int kTilesPerCta = 1;         // tiles per persistent CTA (static round robin)
+constexpr int32_t kMaxTileChunks = 256; // chunk partials of one tile live in shared memory
+constexpr int32_t kUpdateSplit = 4;     // K2 work items per tile (dynamically scheduled)
+constexpr int kNormUnroll = LARS_NORM_UNROLL;  // K1 vector groups per lane per iteration
 constexpr int32_t kDefaultMinTile = 4096;
+constexpr int32_t kChunk = 2048;        // elements per warp work item (multiple of 256)
 
 // One contiguous piece of one tensor inside one work tile. begin is a flat element offset,
 // 64-element aligned; len may end on a ragged tensor tail.
@@ -28,9 +43,16 @@ static_assert(sizeof(Seg) == 16, "Seg is uploaded as-is");
 // A work list: the tensors one launch of K1/K2 covers (all tensors for lars_step, the rank's
 // shard for the DP step), cut into ntiles tiles of (nearly) equal element count. Tile t covers
 // segs [tile_seg[t], tile_seg[t+1]); each CTA of K1/K2 owns exactly one tile (static balance).
+// Segments are further cut into warp chunks of <= kChunk elements (Seg records with the same
+// tensor field): tile t's chunks are [tile_chunk[t], tile_chunk[t+1]), segment s's chunks are
+// [seg_chunk[s], seg_chunk[s+1]). The warps of a CTA stream chunks independently, so a tile of
+// fifty 64-element BN vectors costs one memory round trip, not fifty.
 struct WorkList {
   std::vector<Seg> segs;            // flat order
   std::vector<int32_t> tile_seg;    // ntiles + 1
+  std::vector<Seg> chunks;          // flat order
+  std::vector<int32_t> tile_chunk;  // ntiles + 1
+  std::vector<int32_t> seg_chunk;   // nsegs + 1
   std::vector<int32_t> tensors;     // local -> global tensor id
   std::vector<int32_t> tseg_begin;  // local tensor -> first segment (segments are contiguous)
   std::vector<int32_t> tseg_count;  // local tensor -> number of segments
@@ -61,14 +83,25 @@ WorkList make_worklist(const Plan& plan, int32_t rank, int32_t ntiles_target, in
 struct DevWork {
   const Seg* segs;
   const int32_t* tile_seg;
+  const Seg* chunks;
+  const int32_t* tile_chunk;
+  const int32_t* seg_chunk;
   const int32_t* tseg_begin;
   const int32_t* tseg_count;
   const int32_t* tlars;
   int32_t ntiles;
   int32_t ntensors;
+  int32_t grid;      // K1 CTAs: one per tile
+  int32_t upd_grid;  // K2 persistent CTAs: min(ntiles * kUpdateSplit, SMs * kUpdCtasPerSm)
 };
 
 struct DevScratch {
+  // Tile tickets of K1 ([0]) and K2 ([1]): monotonically increasing, never reset. A launch performs
+  // exactly ntiles + grid fetches (one failing fetch per CTA), so ticket % (ntiles + grid) is the
+  // tile index within the launch — CUDA-graph safe, no per-step memset.
+  unsigned long long* ticket;
+  double* cpart_w;       // per chunk: sum w^2 of the chunk
+  double* cpart_g;       // per chunk: sum g^2
   double* part_w;        // per segment: sum w^2 of the segment
   double* part_g;        // per segment: sum g^2
   unsigned* seg_done;    // per local tensor: segments finished this step (reset by the finisher)

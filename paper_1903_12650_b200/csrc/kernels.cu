@@ -115,6 +115,33 @@ template <> struct Grad<LARS_BF16> {
   }
 };
 
+#ifdef LARS_TRACE
+// Diagnostics build only (tools/trace_build.py): per-CTA [start ns, end ns, smid, tiles] per kernel.
+__device__ unsigned long long* g_trace = nullptr;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
+#define TRACE_BEGIN unsigned long long _t0 = gtimer();
+#define TRACE_END(k)                                                          \
+  if (threadIdx.x == 0 && g_trace) {                                          \
+    unsigned long long* _p = g_trace + ((size_t)(k) * 4096 + blockIdx.x) * 4; \
+    _p[0] = _t0; _p[1] = gtimer(); _p[2] = smid(); _p[3] = gridDim.x;         \
+  }
+extern "C" int lars_trace_arm(void* buf) {
+  return (int)cudaMemcpyToSymbol(g_trace, &buf, sizeof buf);
+}
+#else
+#define TRACE_BEGIN
+#define TRACE_END(k)
+#endif
+
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
@@ -124,20 +151,32 @@ __device__ __forceinline__ void acc8(double& a, const F8& x) {
 }
 
 // ---------------------------------------------------------------- K1: segmented norms + finish
-__device__ void finish_tensor(int32_t l, const DevWork& wk, const DevScratch& sc, const Hyper& hy) {
-  // Runs on ONE thread once all segments of local tensor l have published their partials.
-  __threadfence();
-  const int32_t b = wk.tseg_begin[l], c = wk.tseg_count[l];
-  double sw = 0.0, sg = 0.0;
-  for (int32_t i = 0; i < c; ++i) {  // fixed order -> bit-reproducible
-    sw += __ldcg(sc.part_w + b + i);
-    sg += __ldcg(sc.part_g + b + i);
+// Deterministic warp sum of x[a..b): lane i adds elements a+i, a+i+32, ... in order, then a fixed
+// xor butterfly. The result (identical in every lane) depends only on the plan, never on timing.
+__device__ __forceinline__ void warp_sum2(const double* xa, const double* xb, int32_t a, int32_t b, int lane,
+                                          double& ra, double& rb) {
+  double sa = 0.0, sb = 0.0;
+  for (int32_t i = a + lane; i < b; i += 32) {
+    sa += __ldcg(xa + i);
+    sb += __ldcg(xb + i);
   }
-  sc.seg_done[l] = 0u;  // all of this step's arrivals are in: rearm for the next step
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    sb += __shfl_xor_sync(0xffffffffu, sb, o);
+  }
+  ra = sa;
+  rb = sb;
+}
+
+// Per-layer finish from the layer's complete sums: ||w||, ||G|| = |s| sqrt(sum g^2), lambda, lr*lambda.
+// Returns true when a norm is non-finite (the step will be skipped).
+__device__ __forceinline__ bool finish_core(int32_t l, double sw, double sg, const DevWork& wk, const DevScratch& sc,
+                                            const Hyper& hy) {
   const double wn = sqrt(sw);
   const double gn = fabs(hy.grad_scale) * sqrt(sg);
   double lam = 1.0, beta = 0.0;
-  if (wk.tlars[l]) {
+  if (wk.tlars[l]) {  // weight kind: trust ratio + decay (reading #1, #3); skip kinds keep 1, 0 (#4)
     beta = hy.weight_decay;
     const double den = gn + hy.weight_decay * wn + hy.eps;
     if (wn > 0.0 && den > 0.0) lam = hy.eta * wn / den;
@@ -147,72 +186,154 @@ __device__ void finish_tensor(int32_t l, const DevWork& wk, const DevScratch& sc
   sc.lambda[l] = lam;
   sc.coef[l] = (float)(hy.lr_table[hy.iter] * lam);
   sc.beta[l] = (float)beta;
-  if (!(isfinite(wn) && isfinite(gn))) atomicOr(sc.nonfinite, 1u);
-  __threadfence();
-  if (atomicAdd(sc.tensors_done, 1u) == (unsigned)wk.ntensors - 1u) {
-    __threadfence();
-    const unsigned nf = atomicExch(sc.nonfinite, 0u);
-    *(volatile int32_t*)sc.skip = nf ? 1 : 0;
-    *(volatile unsigned*)sc.tensors_done = 0u;
-  }
+  return !(isfinite(wn) && isfinite(gn));
 }
 
 template <int DT>
-__global__ void __launch_bounds__(kThreads) lars_norms_kernel(DevWork wk, DevScratch sc, Hyper hy,
-                                                              const float* __restrict__ w,
-                                                              const void* __restrict__ g, int64_t g_shift) {
-  __shared__ double red_w[kThreads / 32], red_g[kThreads / 32];
-  pdl_trigger();
-  pdl_wait();
+__device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, const DevScratch& sc, const Hyper& hy,
+                                           const float* __restrict__ w, const void* __restrict__ g,
+                                           int64_t g_shift, double* sm_cw, double* sm_cg, unsigned* sm_done,
+                                           unsigned* sm_nonfinite) {
+  constexpr int kWarps = kThreads / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int32_t s0 = wk.tile_seg[blockIdx.x], s1 = wk.tile_seg[blockIdx.x + 1];
-  for (int32_t s = s0; s < s1; ++s) {
-    const Seg sg = wk.segs[s];
-    const float* wp = w + sg.begin;
-    const int64_t gi = sg.begin - g_shift;
-    const int32_t ng = sg.len >> 3;
+  // Phase A: the warps of the CTA stream the tile's chunks independently (no block barrier per layer);
+  // chunk partials stay in shared memory.
+  const int32_t c0 = wk.tile_chunk[tile], c1 = wk.tile_chunk[tile + 1];
+  for (int32_t c = c0 + warp; c < c1; c += kWarps) {
+    const Seg ck = wk.chunks[c];
+    const float* wp = w + ck.begin;
+    const int64_t gi = ck.begin - g_shift;
+    const int32_t ng = ck.len >> 3;
     double aw = 0.0, ag = 0.0, aw1 = 0.0, ag1 = 0.0;
-    int32_t j = tid;
-    for (; j + 3 * kThreads < ng; j += 4 * kThreads) {
-      F8 w0 = ld8_keep(wp + 8 * j), w1 = ld8_keep(wp + 8 * (j + kThreads));
-      F8 w2 = ld8_keep(wp + 8 * (j + 2 * kThreads)), w3 = ld8_keep(wp + 8 * (j + 3 * kThreads));
-      F8 g0 = Grad<DT>::load8_keep(g, gi + 8 * j), g1 = Grad<DT>::load8_keep(g, gi + 8 * (j + kThreads));
-      F8 g2 = Grad<DT>::load8_keep(g, gi + 8 * (j + 2 * kThreads));
-      F8 g3 = Grad<DT>::load8_keep(g, gi + 8 * (j + 3 * kThreads));
-      acc8(aw, w0); acc8(aw1, w1); acc8(aw, w2); acc8(aw1, w3);
-      acc8(ag, g0); acc8(ag1, g1); acc8(ag, g2); acc8(ag1, g3);
+    int32_t j = lane;
+    for (; j + (kNormUnroll - 1) * 32 < ng; j += kNormUnroll * 32) {
+      F8 wv[kNormUnroll], gv[kNormUnroll];
+#pragma unroll
+      for (int u = 0; u < kNormUnroll; ++u) {  // all loads first: 2*kNormUnroll x 32 B in flight per lane
+        wv[u] = ld8_keep(wp + 8 * (j + u * 32));
+        gv[u] = Grad<DT>::load8_keep(g, gi + 8 * (j + u * 32));
+      }
+#pragma unroll
+      for (int u = 0; u < kNormUnroll; u += 2) {
+        acc8(aw, wv[u]);
+        acc8(ag, gv[u]);
+        if (u + 1 < kNormUnroll) {
+          acc8(aw1, wv[u + 1]);
+          acc8(ag1, gv[u + 1]);
+        }
+      }
     }
-    aw += aw1;
-    ag += ag1;
-    for (; j < ng; j += kThreads) {
-      F8 w0 = ld8_keep(wp + 8 * j);
-      F8 g0 = Grad<DT>::load8_keep(g, gi + 8 * j);
+    for (; j < ng; j += 32) {
+      const F8 w0 = ld8_keep(wp + 8 * j);
+      const F8 g0 = Grad<DT>::load8_keep(g, gi + 8 * j);
       acc8(aw, w0);
       acc8(ag, g0);
     }
-    for (int32_t i = (ng << 3) + tid; i < sg.len; i += kThreads) {  // ragged tensor tail
+    aw += aw1;
+    ag += ag1;
+    for (int32_t i = (ng << 3) + lane; i < ck.len; i += 32) {  // ragged tensor tail (< 8 elements)
       const double x = (double)wp[i], y = (double)Grad<DT>::load1(g, gi + i);
       aw = fma(x, x, aw);
       ag = fma(y, y, ag);
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
+    for (int o = 16; o > 0; o >>= 1) {  // fixed butterfly: deterministic
       aw += __shfl_xor_sync(0xffffffffu, aw, o);
       ag += __shfl_xor_sync(0xffffffffu, ag, o);
     }
-    if (lane == 0) { red_w[warp] = aw; red_g[warp] = ag; }
-    __syncthreads();
-    if (tid == 0) {
-      double tw = 0.0, tg = 0.0;
+    if (lane == 0) {
+      sm_cw[c - c0] = aw;
+      sm_cg[c - c0] = ag;
+    }
+  }
+  __syncthreads();  // every chunk partial of this tile is in shared memory
+  // Phase B: one warp per segment sums its chunk partials (fixed order). A layer that lies inside this
+  // tile is finished right here (no global traffic beyond its outputs); a layer spread over several
+  // tiles publishes the segment partial and the warp that brings in its last segment finishes it.
+  const int32_t s0 = wk.tile_seg[tile], s1 = wk.tile_seg[tile + 1];
+  for (int32_t s = s0 + warp; s < s1; s += kWarps) {
+    const int32_t a = wk.seg_chunk[s] - c0, b = wk.seg_chunk[s + 1] - c0;
+    double tw = 0.0, tg = 0.0;
+    for (int32_t i = a + lane; i < b; i += 32) {
+      tw += sm_cw[i];
+      tg += sm_cg[i];
+    }
 #pragma unroll
-      for (int i = 0; i < kThreads / 32; ++i) { tw += red_w[i]; tg += red_g[i]; }
+    for (int o = 16; o > 0; o >>= 1) {
+      tw += __shfl_xor_sync(0xffffffffu, tw, o);
+      tg += __shfl_xor_sync(0xffffffffu, tg, o);
+    }
+    const int32_t l = wk.segs[s].tensor;
+    const int32_t nseg = wk.tseg_count[l];
+    if (nseg == 1) {
+      if (lane == 0) {
+        if (finish_core(l, tw, tg, wk, sc, hy)) atomicOr(sm_nonfinite, 1u);
+        atomicAdd(sm_done, 1u);
+      }
+      continue;
+    }
+    unsigned prev = 0;
+    if (lane == 0) {
       sc.part_w[s] = tw;
       sc.part_g[s] = tg;
       __threadfence();
-      const unsigned prev = atomicAdd(sc.seg_done + sg.tensor, 1u);
-      if (prev == (unsigned)wk.tseg_count[sg.tensor] - 1u) finish_tensor(sg.tensor, wk, sc, hy);
+      prev = atomicAdd(sc.seg_done + l, 1u);
     }
-    __syncthreads();
+    prev = __shfl_sync(0xffffffffu, prev, 0);
+    if (prev == (unsigned)nseg - 1u) {  // last segment of layer l: this warp finishes it
+      __threadfence();
+      const int32_t sb = wk.tseg_begin[l];
+      double sw = 0.0, sg = 0.0;
+      for (int32_t i = sb + lane; i < sb + nseg; i += 32) {
+        sw += __ldcg(sc.part_w + i);
+        sg += __ldcg(sc.part_g + i);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sw += __shfl_xor_sync(0xffffffffu, sw, o);
+        sg += __shfl_xor_sync(0xffffffffu, sg, o);
+      }
+      if (lane == 0) {
+        sc.seg_done[l] = 0u;  // all of this step's arrivals are in: rearm for the next step
+        if (finish_core(l, sw, sg, wk, sc, hy)) atomicOr(sm_nonfinite, 1u);
+        atomicAdd(sm_done, 1u);
+      }
+    }
+  }
+}
+
+// K1. Static persistent schedule: CTA b owns tiles b, b + grid, ...
+template <int DT>
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_norms_kernel(DevWork wk, DevScratch sc, Hyper hy,
+                                                                          const float* __restrict__ w,
+                                                                          const void* __restrict__ g,
+                                                                          int64_t g_shift) {
+  __shared__ double sm_cw[kMaxTileChunks], sm_cg[kMaxTileChunks];
+  __shared__ unsigned sm_done, sm_nonfinite;
+  pdl_trigger();
+  if (threadIdx.x == 0) {
+    sm_done = 0u;
+    sm_nonfinite = 0u;
+  }
+  pdl_wait();
+  TRACE_BEGIN
+  for (int32_t tile = blockIdx.x; tile < wk.ntiles; tile += gridDim.x) {
+    __syncthreads();  // shared chunk partials of the previous tile fully consumed
+    norms_tile<DT>(tile, wk, sc, hy, w, g, g_shift, sm_cw, sm_cg, &sm_done, &sm_nonfinite);
+  }
+  __syncthreads();
+  TRACE_END(0)
+  // Count this CTA's finished layers once; the CTA that completes the count decides the step's skip.
+  if (threadIdx.x == 0 && sm_done > 0u) {
+    if (sm_nonfinite) atomicOr(sc.nonfinite, 1u);
+    __threadfence();
+    const unsigned before = atomicAdd(sc.tensors_done, sm_done);
+    if (before + sm_done == (unsigned)wk.ntensors) {
+      __threadfence();
+      const unsigned nf = atomicExch(sc.nonfinite, 0u);
+      *(volatile int32_t*)sc.skip = nf ? 1 : 0;
+      *(volatile unsigned*)sc.tensors_done = 0u;
+    }
   }
 }
 
@@ -228,48 +349,87 @@ __device__ __forceinline__ void upd8(F8& w, F8& m, const F8& g, float s, float c
 }
 
 template <int DT>
-__global__ void __launch_bounds__(kThreads) lars_update_kernel(DevWork wk, DevScratch sc, Hyper hy,
-                                                               float* __restrict__ w,
-                                                               const void* __restrict__ g, int64_t g_shift,
-                                                               float* __restrict__ m) {
-  pdl_trigger();
-  pdl_wait();
-  if (*(volatile const int32_t*)sc.skip) return;  // whole step skipped (non-finite norm)
-  const int tid = threadIdx.x;
+__device__ __forceinline__ void update_item(int32_t item, const DevWork& wk, const DevScratch& sc, const Hyper& hy,
+                                            float* __restrict__ w, const void* __restrict__ g, int64_t g_shift,
+                                            float* __restrict__ m) {
+  constexpr int kWarps = kThreads / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float s = hy.grad_scale_f, mu = hy.mu;
-  const int32_t s0 = wk.tile_seg[blockIdx.x], s1 = wk.tile_seg[blockIdx.x + 1];
-  for (int32_t s_ = s1 - 1; s_ >= s0; --s_) {  // backwards: K1's most recent reads first
-    const Seg sg = wk.segs[s_];
-    const float c = sc.coef[sg.tensor], b = sc.beta[sg.tensor];
-    float* wp = w + sg.begin;
-    float* mp = m + sg.begin;
-    const int64_t gi = sg.begin - g_shift;
-    const int32_t ng = sg.len >> 3;
-    for (int32_t i = (ng << 3) + tid; i < sg.len; i += kThreads) {  // ragged tail
-      float wv = wp[i], mv = mp[i];
+  // item -> (part q, tile): all tiles' last parts first (the bytes K1 read last, still in L2), then the
+  // next-to-last parts, ...; inside a part the chunks run backwards.
+  const int32_t q = kUpdateSplit - 1 - item / wk.ntiles, tile = item % wk.ntiles;
+  const int32_t t0 = wk.tile_chunk[tile], tn = wk.tile_chunk[tile + 1] - t0;
+  const int32_t c0 = t0 + (int32_t)((int64_t)tn * q / kUpdateSplit);
+  const int32_t c1 = t0 + (int32_t)((int64_t)tn * (q + 1) / kUpdateSplit);
+  for (int32_t c = c1 - 1 - warp; c >= c0; c -= kWarps) {  // backwards: K1's most recent reads first
+    const Seg ck = wk.chunks[c];
+    const float cf = sc.coef[ck.tensor], b = sc.beta[ck.tensor];
+    float* wp = w + ck.begin;
+    float* mp = m + ck.begin;
+    const int64_t gi = ck.begin - g_shift;
+    const int32_t ng = ck.len >> 3;
+    for (int32_t i = (ng << 3) + lane; i < ck.len; i += 32) {  // ragged tensor tail (< 8 elements)
+      const float wv = wp[i], mv = mp[i];
       const float u = fmaf(b, wv, s * Grad<DT>::load1(g, gi + i));
-      const float v = fmaf(mu, mv, c * u);
+      const float v = fmaf(mu, mv, cf * u);
       wp[i] = wv - v;
       mp[i] = v;
     }
-    int32_t j = ng - 1 - tid;
-    for (; j - kThreads >= 0; j -= 2 * kThreads) {
-      const int32_t j1 = j - kThreads;
+    int32_t j = ng - 1 - lane;
+    for (; j - 32 >= 0; j -= 64) {
+      const int32_t j1 = j - 32;
       F8 w0 = ld8_rw(wp + 8 * j), w1 = ld8_rw(wp + 8 * j1);
-      F8 g0 = Grad<DT>::load8(g, gi + 8 * j), g1 = Grad<DT>::load8(g, gi + 8 * j1);
+      const F8 g0 = Grad<DT>::load8(g, gi + 8 * j), g1 = Grad<DT>::load8(g, gi + 8 * j1);
       F8 m0 = ld8_rw(mp + 8 * j), m1 = ld8_rw(mp + 8 * j1);
-      upd8(w0, m0, g0, s, c, b, mu);
-      upd8(w1, m1, g1, s, c, b, mu);
-      st8(wp + 8 * j, w0); st8(mp + 8 * j, m0);
-      st8(wp + 8 * j1, w1); st8(mp + 8 * j1, m1);
+      upd8(w0, m0, g0, s, cf, b, mu);
+      upd8(w1, m1, g1, s, cf, b, mu);
+      st8(wp + 8 * j, w0);
+      st8(mp + 8 * j, m0);
+      st8(wp + 8 * j1, w1);
+      st8(mp + 8 * j1, m1);
     }
     if (j >= 0) {
-      F8 w0 = ld8_rw(wp + 8 * j), g0 = Grad<DT>::load8(g, gi + 8 * j), m0 = ld8_rw(mp + 8 * j);
-      upd8(w0, m0, g0, s, c, b, mu);
+      F8 w0 = ld8_rw(wp + 8 * j), m0 = ld8_rw(mp + 8 * j);
+      const F8 g0 = Grad<DT>::load8(g, gi + 8 * j);
+      upd8(w0, m0, g0, s, cf, b, mu);
       st8(wp + 8 * j, w0);
       st8(mp + 8 * j, m0);
     }
   }
+}
+
+// K2. Dynamic persistent schedule: ntiles * kUpdateSplit items handed out by a ticket counter, so a
+// CTA that gets less memory bandwidth simply takes fewer items (per-CTA bandwidth on a loaded B200
+// varies by ~1.5x; a static split would wait for the slowest CTA).
+__device__ __forceinline__ int32_t take_ticket(unsigned long long* t, int32_t nitems, int32_t grid) {
+  return (int32_t)(atomicAdd(t, 1ull) % (unsigned long long)(nitems + grid));
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kThreads, kUpdCtasPerSm) lars_update_kernel(DevWork wk, DevScratch sc, Hyper hy,
+                                                                           float* __restrict__ w,
+                                                                           const void* __restrict__ g,
+                                                                           int64_t g_shift, float* __restrict__ m) {
+  __shared__ int32_t s_item;
+  pdl_trigger();
+  pdl_wait();
+  // A skipped step still draws its tickets, keeping the ticket arithmetic of the next launch aligned.
+  const bool skip = *(volatile const int32_t*)sc.skip != 0;  // whole step skipped (non-finite norm)
+  const int32_t nitems = wk.ntiles * kUpdateSplit;
+  TRACE_BEGIN
+  if (threadIdx.x == 0) s_item = take_ticket(sc.ticket + 1, nitems, gridDim.x);
+  __syncthreads();
+  int32_t item = s_item;
+  while (item < nitems) {
+    __syncthreads();  // everyone has read s_item
+    int32_t next = 0;
+    if (threadIdx.x == 0) next = take_ticket(sc.ticket + 1, nitems, gridDim.x);  // consumed one item later
+    if (!skip) update_item<DT>(item, wk, sc, hy, w, g, g_shift, m);
+    if (threadIdx.x == 0) s_item = next;
+    __syncthreads();
+    item = s_item;
+  }
+  TRACE_END(1)
 }
 
 // ---------------------------------------------------------------- launchers
@@ -291,12 +451,12 @@ static cudaError_t launch_pdl(K kernel, int grid, cudaStream_t stream, Args... a
 template <int DT>
 static cudaError_t launch_norms_t(const DevWork& wk, const DevScratch& sc, const Hyper& hy, const float* w,
                                   const void* g, int64_t g_shift, cudaStream_t st) {
-  return launch_pdl(lars_norms_kernel<DT>, wk.ntiles, st, wk, sc, hy, w, g, g_shift);
+  return launch_pdl(lars_norms_kernel<DT>, wk.grid, st, wk, sc, hy, w, g, g_shift);
 }
 template <int DT>
 static cudaError_t launch_update_t(const DevWork& wk, const DevScratch& sc, const Hyper& hy, float* w,
                                    const void* g, int64_t g_shift, float* m, cudaStream_t st) {
-  return launch_pdl(lars_update_kernel<DT>, wk.ntiles, st, wk, sc, hy, w, g, g_shift, m);
+  return launch_pdl(lars_update_kernel<DT>, wk.upd_grid, st, wk, sc, hy, w, g, g_shift, m);
 }
 
 cudaError_t launch_norms(int32_t dt, const DevWork& wk, const DevScratch& sc, const Hyper& hy, const float* w,

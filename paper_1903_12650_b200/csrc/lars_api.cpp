@@ -53,13 +53,15 @@ T* carve(char*& p, size_t n) {
   return r;
 }
 
-lars_status_t upload(DevBufs& b) {
+lars_status_t upload(DevBufs& b, int sms) {
   const WorkList& wl = b.wl;
   const size_t ns = std::max<size_t>(wl.segs.size(), 1), nt = std::max<size_t>(wl.tensors.size(), 1),
-               ntl = wl.tile_seg.size();
+               ntl = wl.tile_seg.size(), nc = std::max<size_t>(wl.chunks.size(), 1);
   size_t bytes = 0;
   auto add = [&](size_t n, size_t sz) { bytes += (n * sz + 255) / 256 * 256; };
   add(ns, sizeof(Seg)); add(ntl, 4); add(nt, 4); add(nt, 4); add(nt, 4);                // work list
+  add(nc, sizeof(Seg)); add(ntl, 4); add(ns + 1, 4); add(nc, 8); add(nc, 8);            // chunks
+  add(2, 8);                                                                            // tickets
   add(ns, 8); add(ns, 8); add(nt, 4); add(1, 4); add(1, 4); add(1, 4);                  // partials, counters
   add(nt, 8); add(nt, 8); add(nt, 8); add(nt, 4); add(nt, 4);                           // outputs
   if (cudaMalloc(&b.mem, bytes) != cudaSuccess) return LARS_ERR_OOM;
@@ -70,6 +72,12 @@ lars_status_t upload(DevBufs& b) {
   int32_t* tsb = carve<int32_t>(p, nt);
   int32_t* tsc = carve<int32_t>(p, nt);
   int32_t* tl = carve<int32_t>(p, nt);
+  Seg* chunks = carve<Seg>(p, nc);
+  int32_t* tile_chunk = carve<int32_t>(p, ntl);
+  int32_t* seg_chunk = carve<int32_t>(p, ns + 1);
+  b.sc.ticket = carve<unsigned long long>(p, 2);
+  b.sc.cpart_w = carve<double>(p, nc);
+  b.sc.cpart_g = carve<double>(p, nc);
   b.sc.part_w = carve<double>(p, ns);
   b.sc.part_g = carve<double>(p, ns);
   b.sc.seg_done = carve<unsigned>(p, nt);
@@ -84,9 +92,14 @@ lars_status_t upload(DevBufs& b) {
   auto cp = [](void* d, const void* s, size_t n) { return n == 0 || cudaMemcpy(d, s, n, cudaMemcpyHostToDevice) == cudaSuccess; };
   if (!(cp(segs, wl.segs.data(), wl.segs.size() * sizeof(Seg)) && cp(tile_seg, wl.tile_seg.data(), ntl * 4) &&
         cp(tsb, wl.tseg_begin.data(), wl.tseg_begin.size() * 4) &&
-        cp(tsc, wl.tseg_count.data(), wl.tseg_count.size() * 4) && cp(tl, wl.tlars.data(), wl.tlars.size() * 4)))
+        cp(tsc, wl.tseg_count.data(), wl.tseg_count.size() * 4) && cp(tl, wl.tlars.data(), wl.tlars.size() * 4) &&
+        cp(chunks, wl.chunks.data(), wl.chunks.size() * sizeof(Seg)) && cp(tile_chunk, wl.tile_chunk.data(), ntl * 4) &&
+        cp(seg_chunk, wl.seg_chunk.data(), wl.seg_chunk.size() * 4)))
     return LARS_ERR_CUDA;
-  b.dw = DevWork{segs, tile_seg, tsb, tsc, tl, wl.ntiles(), (int32_t)wl.tensors.size()};
+  b.dw = DevWork{segs, tile_seg, chunks, tile_chunk, seg_chunk, tsb, tsc, tl, wl.ntiles(), (int32_t)wl.tensors.size(),
+                 std::min<int32_t>(wl.ntiles(), sms * kCtasPerSm),
+                 std::min<int32_t>(wl.ntiles() * kUpdateSplit, sms * kUpdCtasPerSm)};
+  (void)sms;
   return LARS_OK;
 }
 
@@ -208,7 +221,7 @@ lars_status_t lars_init(const lars_tensor_t* tensors, int32_t n, const lars_hpar
     int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0) h->sms = sms;
   }
-  h->full.wl = make_worklist(h->plan, -1, h->sms * kCtasPerSm, min_tile);
+  h->full.wl = make_worklist(h->plan, -1, h->sms * kCtasPerSm * kTilesPerCta, min_tile);
   if (device >= 0) {
     DeviceGuard g(device);
     if (cudaMalloc(&h->lr_d, h->plan.lr.size() * sizeof(double)) != cudaSuccess) { lars_destroy(h); return LARS_ERR_OOM; }
@@ -216,7 +229,7 @@ lars_status_t lars_init(const lars_tensor_t* tensors, int32_t n, const lars_hpar
       lars_destroy(h);
       return LARS_ERR_CUDA;
     }
-    st = upload(h->full);
+    st = upload(h->full, h->sms);
     if (st != LARS_OK) { lars_destroy(h); return st; }
   }
   *out = h;
@@ -346,8 +359,8 @@ lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, cons
   cudaFree(d);
   if (r[0] != h->plan.hash || r[1] != h->plan.hash) return LARS_ERR_LAYOUT;
   const int32_t min_tile = h->hp.tile_elems > 0 ? h->hp.tile_elems : kDefaultMinTile;
-  h->shard.wl = make_worklist(h->plan, rank, h->sms * kCtasPerSm, min_tile);
-  lars_status_t st = upload(h->shard);
+  h->shard.wl = make_worklist(h->plan, rank, h->sms * kCtasPerSm * kTilesPerCta, min_tile);
+  lars_status_t st = upload(h->shard, h->sms);
   if (st != LARS_OK) return st;
   if (cudaMalloc(&h->gred, (size_t)h->plan.S * dtype_size(h->hp.grad_dtype)) != cudaSuccess) return LARS_ERR_OOM;
   CUDA_OR(cudaMemset(h->gred, 0, (size_t)h->plan.S * dtype_size(h->hp.grad_dtype)));

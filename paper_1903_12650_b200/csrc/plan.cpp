@@ -136,17 +136,47 @@ lars_status_t make_plan(const lars_tensor_t* t, int32_t n, const lars_hparams_t&
 // 64-element boundaries, so every segment starts 256-byte aligned for fp32. Every CTA then streams
 // the same number of bytes whatever the tensor-size mix (most ResNet-50 layers are
 // too small to occupy a GPU on their own).
+static WorkList make_worklist_once(const Plan& p, int32_t rank, int32_t ntiles_target, int64_t target);
+
+// One CTA per tile in a single wave: if tensor boundaries or the chunk cap produce more tiles than
+// ntiles_target, the tile size grows until they fit.
+// Tiles are balanced by COST, not elements: a piece of a layer costs its elements plus a fixed
+// latency-equivalent per warp chunk and per segment (a 64-element BN vector still costs a memory round
+// trip and a per-layer finish), so tiles full of small layers hold fewer elements.
+constexpr int64_t kChunkCost = 384, kSegCost = 512;
+
 WorkList make_worklist(const Plan& p, int32_t rank, int32_t ntiles_target, int32_t min_tile) {
+  int64_t cost = 0;
+  for (int32_t l = 0; l < p.L; ++l)
+    if (rank < 0 || p.owner[l] == rank) cost += p.numel[l] + kSegCost + kChunkCost * ((p.numel[l] + kChunk - 1) / kChunk);
+  ntiles_target = std::max(1, ntiles_target);
+  int64_t target = std::max<int64_t>(min_tile, (cost + ntiles_target - 1) / ntiles_target);
+  WorkList wl;
+  for (int it = 0; it < 64; ++it) {
+    wl = make_worklist_once(p, rank, ntiles_target, target);
+    if (wl.ntiles() <= ntiles_target) break;
+    target += std::max<int64_t>(kAlign, target / 32);
+  }
+  return wl;
+}
+
+static WorkList make_worklist_once(const Plan& p, int32_t rank, int32_t ntiles_target, int64_t target) {
   WorkList wl;
   std::vector<int32_t> ids;
   for (int32_t l = 0; l < p.L; ++l)
     if (rank < 0 || p.owner[l] == rank) ids.push_back(l);
   std::stable_sort(ids.begin(), ids.end(), [&](int32_t a, int32_t b) { return p.offset[a] < p.offset[b]; });
   for (int32_t l : ids) wl.elems += p.numel[l];
-  int64_t target = std::max<int64_t>(min_tile, (wl.elems + ntiles_target - 1) / std::max(1, ntiles_target));
-  target = std::min<int64_t>(round_up(target, kAlign), (int64_t)1 << 30);
+  (void)ntiles_target;
+  target = std::min<int64_t>(round_up(std::max<int64_t>(target, kSegCost + kChunkCost + kAlign), kAlign),
+                             (int64_t)1 << 30);
   wl.tile_seg.push_back(0);
-  int64_t fill = 0;
+  int64_t fill = 0, tchunks = 0;  // cost / warp chunks in the open tile
+  auto close_tile = [&]() {
+    wl.tile_seg.push_back((int32_t)wl.segs.size());
+    fill = 0;
+    tchunks = 0;
+  };
   for (size_t li = 0; li < ids.size(); ++li) {
     const int32_t l = ids[li];
     wl.tensors.push_back(l);
@@ -154,25 +184,32 @@ WorkList make_worklist(const Plan& p, int32_t rank, int32_t ntiles_target, int32
     wl.tseg_begin.push_back((int32_t)wl.segs.size());
     int64_t pos = 0;
     while (pos < p.numel[l]) {
-      int64_t room = target - fill;
+      int64_t room = target - fill - kSegCost - kChunkCost;
       int64_t take = std::min<int64_t>(p.numel[l] - pos, room);
+      // a tile's chunk partials live in shared memory: at most kMaxTileChunks chunks per tile
+      take = std::min<int64_t>(take, (kMaxTileChunks - tchunks) * (int64_t)kChunk);
       if (take < p.numel[l] - pos) take = take / kAlign * kAlign;  // interior cut: 64-aligned
       if (take <= 0) {  // tile full
-        wl.tile_seg.push_back((int32_t)wl.segs.size());
-        fill = 0;
+        close_tile();
         continue;
       }
       wl.segs.push_back(Seg{p.offset[l] + pos, (int32_t)take, (int32_t)li});
       pos += take;
-      fill += take;
-      if (fill >= target) {
-        wl.tile_seg.push_back((int32_t)wl.segs.size());
-        fill = 0;
-      }
+      tchunks += (take + kChunk - 1) / kChunk;
+      fill += take + kSegCost + kChunkCost * ((take + kChunk - 1) / kChunk);
+      if (fill >= target || tchunks >= kMaxTileChunks) close_tile();
     }
     wl.tseg_count.push_back((int32_t)wl.segs.size() - wl.tseg_begin.back());
   }
   if (fill > 0 || wl.tile_seg.size() == 1) wl.tile_seg.push_back((int32_t)wl.segs.size());
+  // warp chunks: every segment cut into <= kChunk-element pieces (64-aligned interior cuts)
+  wl.seg_chunk.push_back(0);
+  for (const Seg& sg : wl.segs) {
+    for (int64_t pos = 0; pos < sg.len; pos += kChunk)
+      wl.chunks.push_back(Seg{sg.begin + pos, (int32_t)std::min<int64_t>(kChunk, sg.len - pos), sg.tensor});
+    wl.seg_chunk.push_back((int32_t)wl.chunks.size());
+  }
+  for (int32_t t : wl.tile_seg) wl.tile_chunk.push_back(wl.seg_chunk[t]);
   return wl;
 }
 
