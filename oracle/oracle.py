@@ -180,7 +180,8 @@ def step(kinds: list, hp: HParams, t: int, w: list, g_ranks: list, m: list) -> S
         m_new.append(v)
         m_env.append(abs(hp.momentum) * np.abs(M64[l])
                      + abs(lr * lam[l]) * (absg[l] + abs(beta[l]) * np.abs(W64[l])))
-        w_env.append(np.abs(W64[l]) + np.abs(v))
+        # w - v is computed from |w| and every term of v: its envelope is |w| + E_m (reading #17)
+        w_env.append(np.abs(W64[l]) + m_env[-1])
     return StepResult(w_new, m_new, w_norm, g_norm, list(lam), lr, False, m_env, w_env)
 
 

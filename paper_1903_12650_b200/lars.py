@@ -149,7 +149,7 @@ class _DevView:
     """__cuda_array_interface__ wrapper so torch can view library-owned device memory."""
 
     def __init__(self, ptr: int, n: int, typestr: str):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, True), "version": 3}
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3}
 
 
 class Lars:

@@ -3,7 +3,8 @@
 Tolerance semantics (reading #17, north_star): an element passes when
     |gpu - oracle| <= tol * E
 with E the oracle's magnitude envelope (E_m = mu|m| + |lr*lambda|(|s| sum_r |g_r| + beta_l |w|),
-E_w = |w| + |v_new|); E >= |x| so this is plain relative error whenever nothing cancels. Exact zeros
+E_w = |w| + E_m: w - v is formed from |w| and every term of v); E >= |x| so this is plain relative
+error whenever nothing cancels. Exact zeros
 must be exact. Norms: relative 1e-6 against the oracle norm of the very buffer the kernel read.
 """
 from __future__ import annotations
