@@ -65,6 +65,15 @@ typedef enum {
   LARS_KIND_BN_BETA = 3
 } lars_kind_t;
 
+/* How the flat layout is split into P rank shards (hp.shard_policy). */
+typedef enum {
+  LARS_SHARD_CONTIGUOUS = 0, /* default: layout order, equal shards, <= P-1 layers straddle shard
+                                boundaries (their norms are completed across ranks); the flat layout
+                                (offsets) is the same for every P                                      */
+  LARS_SHARD_LPT = 1         /* whole layers bin-packed (longest processing time): no layer spans ranks,
+                                offsets depend on P, padding grows when one layer exceeds ~N/P          */
+} lars_shard_policy_t;
+
 /* Gradient wire dtype: fp16 is the paper's; bf16 optional; fp32 allowed. */
 typedef enum { LARS_F32 = 0, LARS_F16 = 1, LARS_BF16 = 2 } lars_dtype_t;
 
@@ -89,6 +98,8 @@ typedef struct {
   int32_t grad_dtype;    /* lars_dtype_t of g                                                     */
   int32_t nranks;        /* data-parallel world size P the layout is planned for (default 1)       */
   int32_t tile_elems;    /* minimum work-tile size in elements; 0 = library default                */
+  int32_t shard_policy;  /* lars_shard_policy_t (default LARS_SHARD_CONTIGUOUS)                    */
+  int32_t reserved;      /* must be 0                                                             */
 } lars_hparams_t;
 
 typedef struct lars_ctx* lars_handle_t;
@@ -104,9 +115,9 @@ void lars_hparams_default(lars_hparams_t* hp);
 lars_status_t lars_init(const lars_tensor_t* tensors, int32_t n, const lars_hparams_t* hp,
                         int32_t device, lars_handle_t* out);
 
-/* offsets[n] (elements) of every tensor in the flat buffers, and the flat length. At P > 1 the
- * layout is rank-major: rank r owns [r*S, (r+1)*S) (lars_shard_range) and holds whole tensors
- * assigned by longest-processing-time bin packing. Either output may be NULL. */
+/* offsets[n] (elements) of every tensor in the flat buffers, and the flat length (P * S). Rank r owns
+ * elements [r*S, (r+1)*S) (lars_shard_range); see lars_shard_policy_t for how layers map to shards.
+ * Either output may be NULL. */
 lars_status_t lars_layout(lars_handle_t h, int64_t* offsets, int64_t* padded_numel);
 
 /* Schedule: iterations per epoch, total iterations T, warm-up iterations W. Any output may be NULL. */
@@ -118,7 +129,8 @@ lars_status_t lars_lr_at(lars_handle_t h, int64_t iter, double* lr);
 /* Element range [begin, end) of rank `rank`'s shard (P = 1: the whole flat buffer). */
 lars_status_t lars_shard_range(lars_handle_t h, int32_t rank, int64_t* begin, int64_t* end);
 
-/* owner[n]: the rank that updates each tensor. */
+/* owner[n]: the rank whose shard holds each tensor's first element (a layer that straddles a shard
+ * boundary under LARS_SHARD_CONTIGUOUS is updated piecewise by every rank it touches). */
 lars_status_t lars_tensor_owner(lars_handle_t h, int32_t* owner);
 
 /* 64-bit FNV-1a hash of (layout, hyper-parameters, P); equal on every rank that planned alike. */
@@ -129,6 +141,12 @@ lars_status_t lars_layout_hash(lars_handle_t h, uint64_t* hash);
  * non-finite check) and the fused update kernel (K2: unscale + weight decay + momentum + update,
  * streaming w, g, m once) on `stream`; returns without synchronizing. */
 lars_status_t lars_step(lars_handle_t h, float* w, const void* g, float* m, int64_t iter, void* stream);
+
+/* lars_step with the iteration in DEVICE memory (an aligned int64): K1 reads *iter_dev and, once every layer
+ * has used it, stores *iter_dev + 1 — so one captured CUDA graph replays the whole warm-up + decay schedule
+ * (1,440 updates at B = 81,920). An iteration outside [0, T) is reported on the device:
+ * the step is skipped and lars_last_step_skipped returns 2. */
+lars_status_t lars_step_dev_iter(lars_handle_t h, float* w, const void* g, float* m, int64_t* iter_dev, void* stream);
 
 /* Same as lars_step, but the gradient comes from HOST memory g_host (pinned for async copies,
  * padded_numel elements of grad_dtype): the library copies it into its own device staging buffer on
@@ -154,6 +172,10 @@ lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, cons
 lars_status_t dp_allreduce_lars_step(lars_handle_t h, float* w, const void* g, float* m, int64_t iter,
                                      void* stream);
 
+/* dp_allreduce_lars_step with the iteration in device memory (see lars_step_dev_iter). */
+lars_status_t dp_allreduce_lars_step_dev_iter(lars_handle_t h, float* w, const void* g, float* m, int64_t* iter_dev,
+                                              void* stream);
+
 /* Same as dp_allreduce_lars_step with the rank's local gradient in HOST memory g_host (pinned for async
  * copies, padded_numel elements): H2D copy into a library staging buffer, the dp step, then a D2H copy of
  * the step status + per-layer norms into library-owned pinned memory, all on `stream`. */
@@ -176,6 +198,7 @@ lars_status_t lars_reduced_grad(lars_handle_t h, const void** dev_ptr, int64_t* 
  * left untouched). w_norm = ||w_l||, g_norm = ||G_l|| (grad_scale applied), lambda = trust ratio,
  * coef = lr*lambda as the update kernel used it. Any output may be NULL. */
 lars_status_t lars_last_norms(lars_handle_t h, double* w_norm, double* g_norm, double* lambda, double* coef);
+/* *skipped: 0 = applied, 1 = skipped (non-finite norm), 2 = skipped (device iteration out of range). */
 lars_status_t lars_last_step_skipped(lars_handle_t h, int32_t* skipped);
 
 lars_status_t lars_destroy(lars_handle_t h);

@@ -57,6 +57,7 @@ struct WorkList {
   std::vector<int32_t> tseg_begin;  // local tensor -> first segment (segments are contiguous)
   std::vector<int32_t> tseg_count;  // local tensor -> number of segments
   std::vector<int32_t> tlars;       // local tensor -> 1 if weight kind (LARS + decay)
+  std::vector<int32_t> tsplit;      // local tensor -> global split slot (-1: the layer is whole here)
   int64_t elems = 0;
   int32_t ntiles() const { return (int32_t)tile_seg.size() - 1; }
 };
@@ -65,7 +66,9 @@ struct Plan {
   int32_t L = 0, P = 1;
   std::vector<int64_t> numel;
   std::vector<int32_t> kind;
-  std::vector<int32_t> owner;   // rank per tensor
+  std::vector<int32_t> owner;   // rank holding the tensor's first element
+  std::vector<int32_t> split;   // split slot of a tensor straddling shards (-1: whole on its owner)
+  int32_t nsplit = 0;
   std::vector<int64_t> offset;  // flat offset per tensor
   int64_t S = 0;                // shard length (P = 1: == padded)
   int64_t padded = 0;           // P * S
@@ -89,6 +92,10 @@ struct DevWork {
   const int32_t* tseg_begin;
   const int32_t* tseg_count;
   const int32_t* tlars;
+  const int32_t* tsplit;        // local tensor -> global split slot or -1
+  const int32_t* split_locals;  // local ids of this rank's split layers
+  int32_t nsplit_local;
+  int32_t nsplit_total;         // split layers in the whole plan (C3 payload: 1 + 2 * nsplit_total doubles)
   int32_t ntiles;
   int32_t ntensors;
   int32_t grid;      // K1 CTAs: one per tile
@@ -108,6 +115,10 @@ struct DevScratch {
   unsigned* tensors_done;
   unsigned* nonfinite;
   int32_t* skip;         // 1 if this step was skipped (written by K1's last finisher)
+  // Data-parallel only (nullptr for the whole-layout step): the C3 allreduce payload
+  // [non-finite count, (sum w^2, sum g^2) of each split layer]; K1 fills this rank's share, the finisher
+  // kernel consumes the global sums and zeroes it for the next step.
+  double* c3;
   double* w_norm;        // per local tensor ||w||
   double* g_norm;        // per local tensor ||G|| (grad_scale applied)
   double* lambda;        // trust ratio
@@ -117,7 +128,9 @@ struct DevScratch {
 
 struct Hyper {
   const double* lr_table;
-  int64_t iter;
+  int64_t iter;              // host-given iteration (iter_dev == nullptr)
+  int64_t* iter_dev;         // device iteration: read by K1, advanced by one after the step's last use
+  int64_t total_iters;       // T (device-side range check for iter_dev)
   double eta, weight_decay, eps, grad_scale;
   float mu, grad_scale_f;
 };
@@ -127,6 +140,8 @@ cudaError_t launch_norms(int32_t grad_dtype, const DevWork& wk, const DevScratch
                          const float* w, const void* g, int64_t g_shift, cudaStream_t stream);
 cudaError_t launch_update(int32_t grad_dtype, const DevWork& wk, const DevScratch& sc, const Hyper& hy,
                           float* w, const void* g, int64_t g_shift, float* m, cudaStream_t stream);
+// After the C3 allreduce: finish split layers, decide the global skip, advance a device iteration.
+cudaError_t launch_split_finish(const DevWork& wk, const DevScratch& sc, const Hyper& hy, cudaStream_t stream);
 cudaError_t launch_step(int32_t grad_dtype, const DevWork& wk, const DevScratch& sc, const Hyper& hy,
                         float* w, const void* g, int64_t g_shift, float* m, cudaStream_t stream);
 

@@ -184,9 +184,11 @@ __device__ __forceinline__ bool finish_core(int32_t l, double sw, double sg, con
   sc.w_norm[l] = wn;
   sc.g_norm[l] = gn;
   sc.lambda[l] = lam;
-  sc.coef[l] = (float)(hy.lr_table[hy.iter] * lam);
+  const int64_t t = hy.iter_dev ? *(volatile const int64_t*)hy.iter_dev : hy.iter;
+  const bool in_range = t >= 0 && t < hy.total_iters;  // host-given iterations are validated on the host
+  sc.coef[l] = in_range ? (float)(hy.lr_table[t] * lam) : 0.0f;
   sc.beta[l] = (float)beta;
-  return !(isfinite(wn) && isfinite(gn));
+  return !(isfinite(wn) && isfinite(gn) && in_range);
 }
 
 template <int DT>
@@ -265,9 +267,15 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
     }
     const int32_t l = wk.segs[s].tensor;
     const int32_t nseg = wk.tseg_count[l];
+    const int32_t split = wk.tsplit[l];
     if (nseg == 1) {
       if (lane == 0) {
-        if (finish_core(l, tw, tg, wk, sc, hy)) atomicOr(sm_nonfinite, 1u);
+        if (split >= 0) {  // straddles ranks: publish this rank's share for the C3 allreduce
+          sc.c3[1 + 2 * split] = tw;
+          sc.c3[2 + 2 * split] = tg;
+        } else if (finish_core(l, tw, tg, wk, sc, hy)) {
+          atomicOr(sm_nonfinite, 1u);
+        }
         atomicAdd(sm_done, 1u);
       }
       continue;
@@ -295,7 +303,12 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
       }
       if (lane == 0) {
         sc.seg_done[l] = 0u;  // all of this step's arrivals are in: rearm for the next step
-        if (finish_core(l, sw, sg, wk, sc, hy)) atomicOr(sm_nonfinite, 1u);
+        if (split >= 0) {
+          sc.c3[1 + 2 * split] = sw;
+          sc.c3[2 + 2 * split] = sg;
+        } else if (finish_core(l, sw, sg, wk, sc, hy)) {
+          atomicOr(sm_nonfinite, 1u);
+        }
         atomicAdd(sm_done, 1u);
       }
     }
@@ -331,8 +344,18 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_norms_kernel(DevWor
     if (before + sm_done == (unsigned)wk.ntensors) {
       __threadfence();
       const unsigned nf = atomicExch(sc.nonfinite, 0u);
-      *(volatile int32_t*)sc.skip = nf ? 1 : 0;
       *(volatile unsigned*)sc.tensors_done = 0u;
+      if (sc.c3) {  // data parallel: the decision is global, taken after the C3 allreduce
+        *(volatile double*)sc.c3 = nf ? 1.0 : 0.0;
+        return;
+      }
+      int32_t status = nf ? 1 : 0;
+      if (hy.iter_dev) {  // every layer has read the iteration: advance it (graph replays walk the schedule)
+        const int64_t t = *(volatile int64_t*)hy.iter_dev;
+        if (t < 0 || t >= hy.total_iters) status = 2;
+        *(volatile int64_t*)hy.iter_dev = t + 1;
+      }
+      *(volatile int32_t*)sc.skip = status;
     }
   }
 }
@@ -432,6 +455,47 @@ __global__ void __launch_bounds__(kThreads, kUpdCtasPerSm) lars_update_kernel(De
   TRACE_END(1)
 }
 
+// A rank that owns no layer still advances a device iteration and reports its range check.
+__global__ void empty_step_kernel(int64_t* iter_dev, int64_t total_iters, int32_t* skip) {
+  const int64_t t = *iter_dev;
+  *skip = (t < 0 || t >= total_iters) ? 2 : 0;
+  *iter_dev = t + 1;
+}
+
+// Data-parallel finish, after C3 = allreduce(sum) of [non-finite count, split-layer partial sums]:
+// every rank sees the same global sums, so every rank takes the same skip decision (reading #13) and
+// each rank finishes the split layers it touches exactly like K1 finishes whole ones.
+__global__ void lars_split_finish_kernel(DevWork wk, DevScratch sc, Hyper hy) {
+  const int lane = threadIdx.x;
+  const int32_t n = 1 + 2 * wk.nsplit_total;
+  bool bad = false;
+  for (int32_t i = lane; i < n; i += 32) {
+    const double x = sc.c3[i];
+    bad |= (i == 0) ? (x > 0.0) : !isfinite(x);
+  }
+  for (int32_t k = lane; k < wk.nsplit_local; k += 32) {
+    const int32_t l = wk.split_locals[k], j = wk.tsplit[l];
+    bad |= finish_core(l, sc.c3[1 + 2 * j], sc.c3[2 + 2 * j], wk, sc, hy);
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  __syncwarp();
+  for (int32_t i = lane; i < n; i += 32) sc.c3[i] = 0.0;  // next step's shares start from zero
+  if (lane == 0) {
+    int32_t status = bad ? 1 : 0;
+    if (hy.iter_dev) {
+      const int64_t t = *hy.iter_dev;
+      if (t < 0 || t >= hy.total_iters) status = 2;
+      *hy.iter_dev = t + 1;
+    }
+    *sc.skip = status;
+  }
+}
+
+cudaError_t launch_split_finish(const DevWork& wk, const DevScratch& sc, const Hyper& hy, cudaStream_t st) {
+  lars_split_finish_kernel<<<1, 32, 0, st>>>(wk, sc, hy);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- launchers
 template <typename K, typename... Args>
 static cudaError_t launch_pdl(K kernel, int grid, cudaStream_t stream, Args... args) {
@@ -461,7 +525,12 @@ static cudaError_t launch_update_t(const DevWork& wk, const DevScratch& sc, cons
 
 cudaError_t launch_norms(int32_t dt, const DevWork& wk, const DevScratch& sc, const Hyper& hy, const float* w,
                          const void* g, int64_t g_shift, cudaStream_t st) {
-  if (wk.ntensors == 0) return cudaMemsetAsync(sc.skip, 0, sizeof(int32_t), st);
+  if (wk.ntensors == 0) {  // nothing owned (P > number of layers): no norms, but keep the contract
+    if (sc.c3) return cudaSuccess;  // data parallel: the finisher kernel decides (its shares stay 0)
+    if (!hy.iter_dev) return cudaMemsetAsync(sc.skip, 0, sizeof(int32_t), st);
+    empty_step_kernel<<<1, 1, 0, st>>>(hy.iter_dev, hy.total_iters, sc.skip);
+    return cudaGetLastError();
+  }
   switch (dt) {
     case LARS_F32: return launch_norms_t<LARS_F32>(wk, sc, hy, w, g, g_shift, st);
     case LARS_F16: return launch_norms_t<LARS_F16>(wk, sc, hy, w, g, g_shift, st);

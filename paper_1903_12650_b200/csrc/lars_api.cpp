@@ -5,7 +5,8 @@
 //                                                             fp16 on the wire PAPER.md:183;
 //                                                             one multi-MB message PAPER.md:147-153
 //   K1  per-layer norms + trust ratio on the rank's shard
-//   C3  ncclAllReduce(skip flag, max)                           whole-step skip is global (reading #13)
+//   C3  ncclAllReduce([non-finite count, split-layer sums], sum) + finisher kernel: the skip decision is
+//       global (reading #13) and layers straddling shards get their norms from every rank
 //   K2  fused update of the shard
 //   C2  ncclAllGather(w shard -> w)                             every replica holds the owner's fp32 weights
 // Everything is stream-ordered: no host synchronization inside a step (CUDA-graph capturable).
@@ -53,7 +54,7 @@ T* carve(char*& p, size_t n) {
   return r;
 }
 
-lars_status_t upload(DevBufs& b, int sms) {
+lars_status_t upload(DevBufs& b, int sms, int32_t nsplit_total, bool dp) {
   const WorkList& wl = b.wl;
   const size_t ns = std::max<size_t>(wl.segs.size(), 1), nt = std::max<size_t>(wl.tensors.size(), 1),
                ntl = wl.tile_seg.size(), nc = std::max<size_t>(wl.chunks.size(), 1);
@@ -62,6 +63,7 @@ lars_status_t upload(DevBufs& b, int sms) {
   add(ns, sizeof(Seg)); add(ntl, 4); add(nt, 4); add(nt, 4); add(nt, 4);                // work list
   add(nc, sizeof(Seg)); add(ntl, 4); add(ns + 1, 4); add(nc, 8); add(nc, 8);            // chunks
   add(2, 8);                                                                            // tickets
+  add(nt, 4); add(nt, 4); add(dp ? 1 + 2 * (size_t)nsplit_total : 1, 8);                // split layers, C3
   add(ns, 8); add(ns, 8); add(nt, 4); add(1, 4); add(1, 4); add(1, 4);                  // partials, counters
   add(nt, 8); add(nt, 8); add(nt, 8); add(nt, 4); add(nt, 4);                           // outputs
   if (cudaMalloc(&b.mem, bytes) != cudaSuccess) return LARS_ERR_OOM;
@@ -76,6 +78,13 @@ lars_status_t upload(DevBufs& b, int sms) {
   int32_t* tile_chunk = carve<int32_t>(p, ntl);
   int32_t* seg_chunk = carve<int32_t>(p, ns + 1);
   b.sc.ticket = carve<unsigned long long>(p, 2);
+  int32_t* tsplit = carve<int32_t>(p, nt);
+  int32_t* split_locals = carve<int32_t>(p, nt);
+  double* c3 = carve<double>(p, dp ? 1 + 2 * (size_t)nsplit_total : 1);
+  b.sc.c3 = dp ? c3 : nullptr;
+  std::vector<int32_t> locals;
+  for (size_t i = 0; i < wl.tsplit.size(); ++i)
+    if (wl.tsplit[i] >= 0) locals.push_back((int32_t)i);
   b.sc.cpart_w = carve<double>(p, nc);
   b.sc.cpart_g = carve<double>(p, nc);
   b.sc.part_w = carve<double>(p, ns);
@@ -94,9 +103,11 @@ lars_status_t upload(DevBufs& b, int sms) {
         cp(tsb, wl.tseg_begin.data(), wl.tseg_begin.size() * 4) &&
         cp(tsc, wl.tseg_count.data(), wl.tseg_count.size() * 4) && cp(tl, wl.tlars.data(), wl.tlars.size() * 4) &&
         cp(chunks, wl.chunks.data(), wl.chunks.size() * sizeof(Seg)) && cp(tile_chunk, wl.tile_chunk.data(), ntl * 4) &&
-        cp(seg_chunk, wl.seg_chunk.data(), wl.seg_chunk.size() * 4)))
+        cp(seg_chunk, wl.seg_chunk.data(), wl.seg_chunk.size() * 4) &&
+        cp(tsplit, wl.tsplit.data(), wl.tsplit.size() * 4) && cp(split_locals, locals.data(), locals.size() * 4)))
     return LARS_ERR_CUDA;
-  b.dw = DevWork{segs, tile_seg, chunks, tile_chunk, seg_chunk, tsb, tsc, tl, wl.ntiles(), (int32_t)wl.tensors.size(),
+  b.dw = DevWork{segs, tile_seg, chunks, tile_chunk, seg_chunk, tsb, tsc, tl, tsplit, split_locals,
+                 (int32_t)locals.size(), dp ? nsplit_total : 0, wl.ntiles(), (int32_t)wl.tensors.size(),
                  std::min<int32_t>(wl.ntiles(), sms * kCtasPerSm),
                  std::min<int32_t>(wl.ntiles() * kUpdateSplit, sms * kUpdCtasPerSm)};
   (void)sms;
@@ -229,7 +240,7 @@ lars_status_t lars_init(const lars_tensor_t* tensors, int32_t n, const lars_hpar
       lars_destroy(h);
       return LARS_ERR_CUDA;
     }
-    st = upload(h->full, h->sms);
+    st = upload(h->full, h->sms, 0, false);
     if (st != LARS_OK) { lars_destroy(h); return st; }
   }
   *out = h;
@@ -285,17 +296,14 @@ static lars_status_t check_step_args(lars_handle_t h, const void* w, const void*
   return LARS_OK;
 }
 
-static Hyper hyper(lars_handle_t h, int64_t iter) {
-  return Hyper{h->lr_d, iter, h->hp.eta, h->hp.weight_decay, h->hp.eps, h->hp.grad_scale,
+static Hyper hyper(lars_handle_t h, int64_t iter, int64_t* iter_dev = nullptr) {
+  return Hyper{h->lr_d, iter, iter_dev, h->plan.T, h->hp.eta, h->hp.weight_decay, h->hp.eps, h->hp.grad_scale,
                (float)h->hp.momentum, (float)h->hp.grad_scale};
 }
 
-lars_status_t lars_step(lars_handle_t h, float* w, const void* g, float* m, int64_t iter, void* stream) {
-  lars_status_t st = check_step_args(h, w, g, m, iter);
-  if (st != LARS_OK) return st;
+static lars_status_t step_impl(lars_handle_t h, float* w, const void* g, float* m, const Hyper& hy, void* stream) {
   DeviceGuard dg(h->device);
   cudaStream_t s = (cudaStream_t)stream;
-  const Hyper hy = hyper(h, iter);
   auto* pe = h->prof.begin(1);
   prof_rec(pe, 0, s);
   CUDA_OR(launch_norms(h->hp.grad_dtype, h->full.dw, h->full.sc, hy, w, g, 0, s));       // K1
@@ -305,6 +313,19 @@ lars_status_t lars_step(lars_handle_t h, float* w, const void* g, float* m, int6
   h->last_stream = s;
   h->last = &h->full;
   return LARS_OK;
+}
+
+lars_status_t lars_step(lars_handle_t h, float* w, const void* g, float* m, int64_t iter, void* stream) {
+  lars_status_t st = check_step_args(h, w, g, m, iter);
+  if (st != LARS_OK) return st;
+  return step_impl(h, w, g, m, hyper(h, iter), stream);
+}
+
+lars_status_t lars_step_dev_iter(lars_handle_t h, float* w, const void* g, float* m, int64_t* iter_dev, void* stream) {
+  if (!iter_dev || ((uintptr_t)iter_dev & 7u)) return LARS_ERR_INVALID_ARG;
+  lars_status_t st = check_step_args(h, w, g, m, 0);
+  if (st != LARS_OK) return st;
+  return step_impl(h, w, g, m, hyper(h, 0, iter_dev), stream);
 }
 
 static lars_status_t stage_host_grad(lars_handle_t h, const void* g_host, cudaStream_t s);
@@ -360,7 +381,7 @@ lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, cons
   if (r[0] != h->plan.hash || r[1] != h->plan.hash) return LARS_ERR_LAYOUT;
   const int32_t min_tile = h->hp.tile_elems > 0 ? h->hp.tile_elems : kDefaultMinTile;
   h->shard.wl = make_worklist(h->plan, rank, h->sms * kCtasPerSm * kTilesPerCta, min_tile);
-  lars_status_t st = upload(h->shard, h->sms);
+  lars_status_t st = upload(h->shard, h->sms, h->plan.nsplit, true);
   if (st != LARS_OK) return st;
   if (cudaMalloc(&h->gred, (size_t)h->plan.S * dtype_size(h->hp.grad_dtype)) != cudaSuccess) return LARS_ERR_OOM;
   CUDA_OR(cudaMemset(h->gred, 0, (size_t)h->plan.S * dtype_size(h->hp.grad_dtype)));
@@ -368,23 +389,21 @@ lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, cons
   return LARS_OK;
 }
 
-lars_status_t dp_allreduce_lars_step(lars_handle_t h, float* w, const void* g, float* m, int64_t iter,
-                                     void* stream) {
-  lars_status_t st = check_step_args(h, w, g, m, iter);
-  if (st != LARS_OK) return st;
+static lars_status_t dp_impl(lars_handle_t h, float* w, const void* g, float* m, const Hyper& hy, void* stream) {
   if (!h->comm || !h->shard_ready) return LARS_ERR_NO_COMM;
   DeviceGuard dg(h->device);
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t S = h->plan.S, begin = (int64_t)h->rank * S;
   const int32_t dt = h->hp.grad_dtype;
-  const Hyper hy = hyper(h, iter);
   auto* pe = h->prof.begin(2);
   prof_rec(pe, 0, s);
   NCCL_OR(ncclReduceScatter(g, h->gred, (size_t)S, nccl_type(dt), ncclSum, h->comm, s));          // C1
   prof_rec(pe, 1, s);
   CUDA_OR(launch_norms(dt, h->shard.dw, h->shard.sc, hy, w, h->gred, begin, s));                   // K1
   prof_rec(pe, 2, s);
-  NCCL_OR(ncclAllReduce(h->shard.sc.skip, h->shard.sc.skip, 1, ncclInt32, ncclMax, h->comm, s));  // C3
+  NCCL_OR(ncclAllReduce(h->shard.sc.c3, h->shard.sc.c3, 1 + 2 * (size_t)h->plan.nsplit, ncclFloat64, ncclSum,
+                        h->comm, s));                                                             // C3
+  CUDA_OR(launch_split_finish(h->shard.dw, h->shard.sc, hy, s));
   prof_rec(pe, 3, s);
   CUDA_OR(launch_update(dt, h->shard.dw, h->shard.sc, hy, w, h->gred, begin, m, s));               // K2
   prof_rec(pe, 4, s);
@@ -393,6 +412,21 @@ lars_status_t dp_allreduce_lars_step(lars_handle_t h, float* w, const void* g, f
   h->last_stream = s;
   h->last = &h->shard;
   return LARS_OK;
+}
+
+lars_status_t dp_allreduce_lars_step(lars_handle_t h, float* w, const void* g, float* m, int64_t iter,
+                                     void* stream) {
+  lars_status_t st = check_step_args(h, w, g, m, iter);
+  if (st != LARS_OK) return st;
+  return dp_impl(h, w, g, m, hyper(h, iter), stream);
+}
+
+lars_status_t dp_allreduce_lars_step_dev_iter(lars_handle_t h, float* w, const void* g, float* m, int64_t* iter_dev,
+                                              void* stream) {
+  if (!iter_dev || ((uintptr_t)iter_dev & 7u)) return LARS_ERR_INVALID_ARG;
+  lars_status_t st = check_step_args(h, w, g, m, 0);
+  if (st != LARS_OK) return st;
+  return dp_impl(h, w, g, m, hyper(h, 0, iter_dev), stream);
 }
 
 static lars_status_t stage_host_grad(lars_handle_t h, const void* g_host, cudaStream_t s) {

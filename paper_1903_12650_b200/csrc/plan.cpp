@@ -54,20 +54,31 @@ static lars_status_t make_schedule(const lars_hparams_t& hp, Plan& p) {
 }
 
 // ---- layout ---------------------------------------------------------------------------------
-// P = 1: tensors in the given order, each at a 64-element aligned offset.
-// P > 1: whole-tensor longest-processing-time bin packing (ties: larger tensor first, then lower
-// index; equal loads -> lower rank), rank-major: rank r owns [r*S, (r+1)*S), tensors inside a shard
-// in index order. No tensor spans ranks, so every per-layer norm is local (SURVEY.md §8(e) "D1").
-static void make_layout(Plan& p) {
+// P = 1, and P > 1 with LARS_SHARD_CONTIGUOUS (default): tensors in the given order, each at a
+//   64-element aligned offset — the SAME flat layout for every P. Rank r owns [r*S, (r+1)*S) with
+//   S = ceil(total/P) (64-aligned): perfectly balanced; at most P-1 tensors straddle a shard boundary
+//   ("split" layers, whose norms are completed across ranks by the C3 allreduce).
+// P > 1 with LARS_SHARD_LPT: whole-tensor longest-processing-time bin packing (ties: larger tensor
+//   first, then lower index; equal loads -> lower rank), rank-major, tensors inside a shard in index
+//   order; no layer spans ranks (SURVEY.md §8(e) "D1"), padding grows when a layer exceeds ~N/P.
+static void make_layout(Plan& p, int32_t policy) {
   const int32_t L = p.L, P = p.P;
   std::vector<int64_t> asz(L);
   for (int32_t l = 0; l < L; ++l) asz[l] = round_up(p.numel[l], kAlign);
   p.owner.assign(L, 0);
   p.offset.assign(L, 0);
-  if (P == 1) {
+  p.split.assign(L, -1);
+  p.nsplit = 0;
+  if (P == 1 || policy == LARS_SHARD_CONTIGUOUS) {
     int64_t off = 0;
     for (int32_t l = 0; l < L; ++l) { p.offset[l] = off; off += asz[l]; }
-    p.S = p.padded = std::max<int64_t>(off, kAlign);
+    const int64_t total = std::max<int64_t>(off, kAlign);
+    p.S = round_up((total + P - 1) / P, kAlign);
+    p.padded = p.S * P;
+    for (int32_t l = 0; l < L; ++l) {
+      p.owner[l] = (int32_t)(p.offset[l] / p.S);
+      if ((p.offset[l] + p.numel[l] - 1) / p.S != p.offset[l] / p.S) p.split[l] = p.nsplit++;
+    }
     return;
   }
   std::vector<int32_t> order(L);
@@ -99,6 +110,7 @@ static uint64_t fnv1a(uint64_t h, const void* data, size_t n) {
 }
 
 lars_status_t make_plan(const lars_tensor_t* t, int32_t n, const lars_hparams_t& hp, Plan& p) {
+  if (hp.shard_policy != LARS_SHARD_CONTIGUOUS && hp.shard_policy != LARS_SHARD_LPT) return LARS_ERR_INVALID_ARG;
   if (n <= 0 || t == nullptr) return LARS_ERR_LAYOUT;
   lars_status_t st = validate_hparams(hp);
   if (st != LARS_OK) return st;
@@ -114,7 +126,7 @@ lars_status_t make_plan(const lars_tensor_t* t, int32_t n, const lars_hparams_t&
   }
   st = make_schedule(hp, p);
   if (st != LARS_OK) return st;
-  make_layout(p);
+  make_layout(p, hp.shard_policy);
   uint64_t h = 1469598103934665603ull;
   h = fnv1a(h, &p.L, sizeof p.L);
   h = fnv1a(h, &p.P, sizeof p.P);
@@ -124,7 +136,7 @@ lars_status_t make_plan(const lars_tensor_t* t, int32_t n, const lars_hparams_t&
   const double hd[] = {hp.base_lr, hp.eta, hp.momentum, hp.weight_decay, hp.eps, hp.warmup_epochs,
                        hp.poly_power, hp.grad_scale};
   h = fnv1a(h, hd, sizeof hd);
-  const int64_t hi[] = {hp.global_batch, hp.dataset_size, hp.total_epochs, hp.grad_dtype};
+  const int64_t hi[] = {hp.global_batch, hp.dataset_size, hp.total_epochs, hp.grad_dtype, hp.shard_policy};
   h = fnv1a(h, hi, sizeof hi);
   p.hash = h;
   return LARS_OK;
@@ -136,6 +148,16 @@ lars_status_t make_plan(const lars_tensor_t* t, int32_t n, const lars_hparams_t&
 // 64-element boundaries, so every segment starts 256-byte aligned for fp32. Every CTA then streams
 // the same number of bytes whatever the tensor-size mix (most ResNet-50 layers are
 // too small to occupy a GPU on their own).
+// The part of tensor l inside rank `rank`'s shard, as tensor-relative [lo, hi) (rank < 0: all of it).
+static void piece(const Plan& p, int32_t l, int32_t rank, int64_t& lo, int64_t& hi) {
+  lo = 0;
+  hi = p.numel[l];
+  if (rank < 0) return;
+  const int64_t b = (int64_t)rank * p.S, e = b + p.S;
+  lo = std::max<int64_t>(0, b - p.offset[l]);
+  hi = std::min<int64_t>(p.numel[l], e - p.offset[l]);
+}
+
 static WorkList make_worklist_once(const Plan& p, int32_t rank, int32_t ntiles_target, int64_t target);
 
 // One CTA per tile in a single wave: if tensor boundaries or the chunk cap produce more tiles than
@@ -147,8 +169,11 @@ constexpr int64_t kChunkCost = 384, kSegCost = 512;
 
 WorkList make_worklist(const Plan& p, int32_t rank, int32_t ntiles_target, int32_t min_tile) {
   int64_t cost = 0;
-  for (int32_t l = 0; l < p.L; ++l)
-    if (rank < 0 || p.owner[l] == rank) cost += p.numel[l] + kSegCost + kChunkCost * ((p.numel[l] + kChunk - 1) / kChunk);
+  for (int32_t l = 0; l < p.L; ++l) {
+    int64_t lo, hi;
+    piece(p, l, rank, lo, hi);
+    if (hi > lo) cost += (hi - lo) + kSegCost + kChunkCost * ((hi - lo + kChunk - 1) / kChunk);
+  }
   ntiles_target = std::max(1, ntiles_target);
   int64_t target = std::max<int64_t>(min_tile, (cost + ntiles_target - 1) / ntiles_target);
   WorkList wl;
@@ -163,10 +188,17 @@ WorkList make_worklist(const Plan& p, int32_t rank, int32_t ntiles_target, int32
 static WorkList make_worklist_once(const Plan& p, int32_t rank, int32_t ntiles_target, int64_t target) {
   WorkList wl;
   std::vector<int32_t> ids;
-  for (int32_t l = 0; l < p.L; ++l)
-    if (rank < 0 || p.owner[l] == rank) ids.push_back(l);
+  for (int32_t l = 0; l < p.L; ++l) {
+    int64_t lo, hi;
+    piece(p, l, rank, lo, hi);
+    if (hi > lo) ids.push_back(l);
+  }
   std::stable_sort(ids.begin(), ids.end(), [&](int32_t a, int32_t b) { return p.offset[a] < p.offset[b]; });
-  for (int32_t l : ids) wl.elems += p.numel[l];
+  for (int32_t l : ids) {
+    int64_t lo, hi;
+    piece(p, l, rank, lo, hi);
+    wl.elems += hi - lo;
+  }
   (void)ntiles_target;
   target = std::min<int64_t>(round_up(std::max<int64_t>(target, kSegCost + kChunkCost + kAlign), kAlign),
                              (int64_t)1 << 30);
@@ -181,14 +213,16 @@ static WorkList make_worklist_once(const Plan& p, int32_t rank, int32_t ntiles_t
     const int32_t l = ids[li];
     wl.tensors.push_back(l);
     wl.tlars.push_back(p.kind[l] == LARS_KIND_WEIGHT ? 1 : 0);
+    wl.tsplit.push_back(rank < 0 ? -1 : p.split[l]);  // a whole-layout step sees every layer whole
     wl.tseg_begin.push_back((int32_t)wl.segs.size());
-    int64_t pos = 0;
-    while (pos < p.numel[l]) {
+    int64_t pos, end;
+    piece(p, l, rank, pos, end);
+    while (pos < end) {
       int64_t room = target - fill - kSegCost - kChunkCost;
-      int64_t take = std::min<int64_t>(p.numel[l] - pos, room);
+      int64_t take = std::min<int64_t>(end - pos, room);
       // a tile's chunk partials live in shared memory: at most kMaxTileChunks chunks per tile
       take = std::min<int64_t>(take, (kMaxTileChunks - tchunks) * (int64_t)kChunk);
-      if (take < p.numel[l] - pos) take = take / kAlign * kAlign;  // interior cut: 64-aligned
+      if (take < end - pos) take = take / kAlign * kAlign;  // interior cut: 64-aligned
       if (take <= 0) {  // tile full
         close_tile();
         continue;

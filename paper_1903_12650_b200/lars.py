@@ -22,6 +22,7 @@ HEADER = os.path.join(os.path.dirname(PKG), "include", "lars.h")
 KIND = {"weight": 0, "bias": 1, "bn_gamma": 2, "bn_beta": 3}
 DTYPE = {"f32": 0, "f16": 1, "bf16": 2}
 DTYPE_BYTES = {"f32": 4, "f16": 2, "bf16": 2}
+SHARD_POLICY = {"contiguous": 0, "lpt": 1}
 
 
 class LarsLibraryMissing(RuntimeError):
@@ -43,7 +44,7 @@ class HParams(ctypes.Structure):
                 ("eps", c_double), ("warmup_epochs", c_double), ("poly_power", c_double),
                 ("grad_scale", c_double), ("global_batch", c_int64), ("dataset_size", c_int64),
                 ("total_epochs", c_int32), ("grad_dtype", c_int32), ("nranks", c_int32),
-                ("tile_elems", c_int32)]
+                ("tile_elems", c_int32), ("shard_policy", c_int32), ("reserved", c_int32)]
 
 
 _lib = None
@@ -69,6 +70,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "lars_layout_hash": (c_int32, [h, POINTER(c_uint64)]),
         "lars_step": (c_int32, [h, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
         "lars_step_host_grad": (c_int32, [h, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
+        "lars_step_dev_iter": (c_int32, [h, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+        "dp_allreduce_lars_step_dev_iter": (c_int32, [h, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
         "lars_get_unique_id": (c_int32, [c_void_p]),
         "lars_comm_init": (c_int32, [h, c_int32, c_int32, c_void_p]),
         "dp_allreduce_lars_step": (c_int32, [h, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
@@ -135,6 +138,8 @@ def default_hparams(**kw) -> HParams:
     for k, v in kw.items():
         if k == "grad_dtype" and isinstance(v, str):
             v = DTYPE[v]
+        if k == "shard_policy" and isinstance(v, str):
+            v = SHARD_POLICY[v]
         setattr(hp, k, v)
     return hp
 
@@ -206,6 +211,15 @@ class Lars:
 
     step = lars_step
 
+    def lars_step_dev_iter(self, w, g, m, iter_dev, stream=None) -> None:
+        """iter_dev: an int64 device tensor (or address); advanced by one by the step itself."""
+        _check(self._lib.lars_step_dev_iter(self._h, _ptr(w), _ptr(g), _ptr(m), _ptr(iter_dev), _stream(stream)),
+               "lars_step_dev_iter")
+
+    def dp_allreduce_lars_step_dev_iter(self, w, g, m, iter_dev, stream=None) -> None:
+        _check(self._lib.dp_allreduce_lars_step_dev_iter(self._h, _ptr(w), _ptr(g), _ptr(m), _ptr(iter_dev),
+                                                         _stream(stream)), "dp_allreduce_lars_step_dev_iter")
+
     def lars_step_host_grad(self, w, g_host, m, it: int, stream=None) -> None:
         _check(self._lib.lars_step_host_grad(self._h, _ptr(w), _ptr(g_host), _ptr(m), it, _stream(stream)),
                "lars_step_host_grad")
@@ -265,10 +279,14 @@ class Lars:
         _check(self._lib.lars_last_norms(self._h, a, b, c, d), "lars_last_norms")
         return list(a), list(b), list(c), list(d)
 
-    def last_step_skipped(self) -> bool:
+    def last_step_status(self) -> int:
+        """0 applied, 1 skipped (non-finite norm), 2 skipped (device iteration out of range)."""
         x = c_int32()
         _check(self._lib.lars_last_step_skipped(self._h, byref(x)), "lars_last_step_skipped")
-        return bool(x.value)
+        return int(x.value)
+
+    def last_step_skipped(self) -> bool:
+        return self.last_step_status() != 0
 
     def close(self) -> None:
         if getattr(self, "_h", None):

@@ -56,9 +56,14 @@ def main():
             g_all = [G.integer_grads(lay, r, t, dtype) for r in range(P)]
         else:
             g_all = [G.grads(lay, r, t, dtype) for r in range(P)]
-        if inject_nan and rank == 1 % P:
-            g_all[rank][0] = g_all[rank][0].copy()
-            g_all[rank][0][3] = np.nan
+        if inject_nan:  # rank 1 poisons one element of ITS local gradient
+            q, l0, i0 = 1 % P, 0, 3
+            if inject_nan == "split":  # ... the last element of a layer that straddles a shard boundary
+                S = h.padded_numel // P
+                l0 = next(l for l, x in enumerate(lay) if h.offsets[l] // S != (h.offsets[l] + x.numel - 1) // S)
+                i0 = lay[l0].numel - 1
+            g_all[q][l0] = g_all[q][l0].copy()
+            g_all[q][l0][i0] = np.nan
         pack = lambda a: torch.from_numpy(G.pack(a, h.offsets, h.padded_numel).view(
             np.int16 if a[0].dtype == np.uint16 else a[0].dtype)).to(dev)
         w, g, m = pack(w_l), pack(g_all[rank]), pack(m_l)
@@ -66,61 +71,67 @@ def main():
         h.dp_allreduce_lars_step(w, g, m, t)
         torch.cuda.synchronize()
         res = {"name": name, "dtype": dtype, "t": t}
-        same = all_same(w)  # collective: every rank calls it before any rank-local assertion
+        same = all_same(w)  # collectives first: every rank calls them before any rank-local assertion
+        red_t, b, e = h.reduced_grad()
+        parts = [torch.empty_like(red_t) for _ in range(P)]
+        dist.all_gather(parts, red_t.clone())
+        full_red = from_dev(torch.cat(parts))  # the exact buffer every K1 read, all shards
         assert torch.equal(g.view(torch.int16) if g.element_size() == 2 else g.view(torch.int32),
                            g_before.view(torch.int16) if g.element_size() == 2 else g_before.view(torch.int32)), \
             "dp step modified the caller's gradient"
         assert same, f"{name}: w differs across ranks after the all-gather"
-        skipped = h.last_step_skipped()
-        owner = h.tensor_owner()
-        mine = [l for l in range(len(lay)) if owner[l] == rank]
+        status = h.last_step_status()
         sizes = [x.numel for x in lay]
+        # this rank's piece of every layer (layers may straddle shard boundaries)
+        pieces = {}
+        for l in range(len(lay)):
+            lo, hi = max(h.offsets[l], b), min(h.offsets[l] + sizes[l], e)
+            if hi > lo:
+                pieces[l] = (lo - h.offsets[l], hi - h.offsets[l])
+        mine = sorted(pieces)
+        res["split_layers_here"] = sum(1 for l in mine if pieces[l] != (0, sizes[l]))
         wg = G.unpack(from_dev(w), h.offsets, sizes)
         mg = G.unpack(from_dev(m), h.offsets, sizes)
         if inject_nan:
-            assert skipped, f"{name}: rank {rank} did not skip although rank 1 had a NaN"
+            assert status == 1, f"{name}: rank {rank} did not skip although rank 1 had a NaN"
             for l in mine:
                 assert np.array_equal(wg[l], w_l[l]) and np.array_equal(mg[l], m_l[l])
             res["skipped_everywhere"] = True
             report["cases"].append(res)
             h.close()
             return
-        assert not skipped
-        # reduced shard vs brute-force sum over ranks
-        red, b, e = h.reduced_grad()
-        red = from_dev(red)
+        assert status == 0
         kinds = [x.kind for x in lay]
-        exact = {l: O.combine([g_all[r][l] for r in range(P)], 1.0) for l in mine}
         worst_sum = 0.0
         for l in mine:
-            got = O.to_double(red[h.offsets[l] - b: h.offsets[l] - b + sizes[l]])
+            lo, hi = pieces[l]
+            got = O.to_double(full_red[h.offsets[l] + lo: h.offsets[l] + hi])
+            exact = O.combine([g_all[r][l][lo:hi] for r in range(P)], 1.0)
             if kind == "integer" and dtype != "bf16":
-                assert np.array_equal(got, exact[l]), f"{name}: integer sum not exact (tensor {l})"
+                assert np.array_equal(got, exact), f"{name}: integer sum not exact (tensor {l})"
             else:
                 bound = (P - 1) * (2.0 ** -11 if dtype == "f16" else 2.0 ** -8 if dtype == "bf16" else 2.0 ** -24) \
-                    * sum(np.abs(O.to_double(g_all[r][l])) for r in range(P))
-                err = np.abs(got - exact[l])
-                ok = err <= bound + 0.0
-                assert ok.all(), f"{name}: reduction error above the (P-1)u sum|g| bound at tensor {l}"
+                    * sum(np.abs(O.to_double(g_all[r][l][lo:hi])) for r in range(P))
+                err = np.abs(got - exact)
+                assert (err <= bound).all(), f"{name}: reduction error above the (P-1)u sum|g| bound at tensor {l}"
                 worst_sum = max(worst_sum, float(np.max(np.where(bound > 0, err / np.maximum(bound, 1e-300), 0))))
         res["sum_err_over_bound"] = worst_sum
-        # norms on the exact buffer K1 read (the reduced shard)
+        # norms (split layers included) on the exact reduced buffer
         hp = oracle_hp(kw)
         wn, gn, lam, coef = h.last_norms()
         s = kw["grad_scale"]
         for l in mine:
-            got_red = red[h.offsets[l] - b: h.offsets[l] - b + sizes[l]]
+            red_l = full_red[h.offsets[l]: h.offsets[l] + sizes[l]]
             gate_norms(f"{name} ||w|| t{l}", [wn[l]], [O.l2norm(w_l[l])])
-            gate_norms(f"{name} ||g|| t{l}", [gn[l]], [abs(s) * O.l2norm(O.to_double(got_red))])
-        # the rank's w/m shard vs the oracle DP step with the exact sum
+            gate_norms(f"{name} ||g|| t{l}", [gn[l]], [abs(s) * O.l2norm(O.to_double(red_l))])
+        # this rank's pieces of w and m vs the oracle DP step (exact sum) of the layers it touches
         r_or = O.dp_step([kinds[l] for l in mine], hp, t, [w_l[l] for l in mine],
                          [[g_all[r][l] for l in mine] for r in range(P)], [m_l[l] for l in mine])
         tol = TOL_F32 if dtype == "f32" else TOL_F16_DP if dtype == "f16" else TOL_BF16_DP
         if mine:
-            res["m_err"] = gate(f"{name} m", np.concatenate([mg[l] for l in mine]), np.concatenate(r_or.m),
-                                np.concatenate(r_or.m_env), tol)
-            res["w_err"] = gate(f"{name} w", np.concatenate([wg[l] for l in mine]), np.concatenate(r_or.w),
-                                np.concatenate(r_or.w_env), tol)
+            sl = lambda arrs: np.concatenate([a[pieces[l][0]:pieces[l][1]] for a, l in zip(arrs, mine)])
+            res["m_err"] = gate(f"{name} m", sl([mg[l] for l in mine]), sl(r_or.m), sl(r_or.m_env), tol)
+            res["w_err"] = gate(f"{name} w", sl([wg[l] for l in mine]), sl(r_or.w), sl(r_or.w_env), tol)
         report["cases"].append(res)
         h.close()
 
@@ -131,7 +142,11 @@ def main():
              ("random-f32", LY.random_layout(np.random.default_rng(9), 23), "f32", 3, {}),
              ("r50-f16", lay_r50, "f16", 719, {}),
              ("r50-int", lay_r50, "f16", 1439, dict(kind="integer")),
-             ("nan-on-rank1", LY.tiny(), "f16", 100, dict(inject_nan=True))]
+             ("r50-lpt-f16", lay_r50, "f16", 80, dict(shard_policy="lpt")),
+             ("zipf-f16", LY.skew1b("zipf", n_tensors=200, total=4_000_000), "f16", 500, {}),
+             ("nan-on-rank1", LY.tiny(), "f16", 100, dict(inject_nan=True)),
+             ("nan-in-split-layer", LY.skew1b("zipf", n_tensors=50, total=1_000_000), "f16", 100,
+              dict(inject_nan="split"))]
     for name, lay, dtype, t, kw in cases:
         ok = 1
         try:

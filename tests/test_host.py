@@ -37,7 +37,7 @@ def test_library_is_sm100a_and_links_torch_nccl():
                                      ("resnet152", 4), ("resnet50_4ch", 1)])
 def test_layout_offsets_aligned_disjoint_and_shards(name, P_):
     lay = LY.by_name(name)
-    h = P.Lars(desc(lay), device=-1, base_lr=32.0, nranks=P_)
+    h = P.Lars(desc(lay), device=-1, base_lr=32.0, nranks=P_, shard_policy="lpt")
     offs, n = np.array(h.offsets), np.array([t.numel for t in lay])
     assert (offs % 64 == 0).all()
     order = np.argsort(offs)
