@@ -174,15 +174,26 @@ def step(kinds: list, hp: HParams, t: int, w: list, g_ranks: list, m: list) -> S
 
     w_new, m_new, m_env, w_env = [], [], [], []
     for l in range(L):
-        u = G[l] + beta[l] * W64[l]                       # g + beta*w
-        v = hp.momentum * M64[l] + lr * lam[l] * u         # v <- mu*v + lr*lambda*(g + beta*w)
-        w_new.append(W64[l] - v)                           # w <- w - v
-        m_new.append(v)
-        m_env.append(abs(hp.momentum) * np.abs(M64[l])
-                     + abs(lr * lam[l]) * (absg[l] + abs(beta[l]) * np.abs(W64[l])))
-        # w - v is computed from |w| and every term of v: its envelope is |w| + E_m (reading #17)
-        w_env.append(np.abs(W64[l]) + m_env[-1])
+        a, b, c, d = update(hp, lr, lam[l], beta[l], W64[l], G[l], M64[l], absg[l])
+        w_new.append(a)
+        m_new.append(b)
+        m_env.append(c)
+        w_env.append(d)
     return StepResult(w_new, m_new, w_norm, g_norm, list(lam), lr, False, m_env, w_env)
+
+
+def update(hp: HParams, lr: float, lam: float, beta: float, w, G, m, abs_g_sum):
+    """O6 for one layer (or any subset of its elements) given its trust ratio lambda and decay beta_l:
+    u = G + beta*w; v = mu*m + lr*lambda*u; w_new = w - v (reading #2). G is the combined, scaled gradient
+    and abs_g_sum = |s| sum_r |g_r| (for the magnitude envelopes of reading #17).
+    Returns (w_new, v, E_m, E_w) in float64."""
+    w = np.asarray(w, dtype=np.float64)
+    m = np.asarray(m, dtype=np.float64)
+    u = G + beta * w                                   # g + beta*w
+    v = hp.momentum * m + lr * lam * u                 # v <- mu*v + lr*lambda*(g + beta*w)
+    e_m = abs(hp.momentum) * np.abs(m) + abs(lr * lam) * (abs_g_sum + abs(beta) * np.abs(w))
+    # w - v is computed from |w| and every term of v: its envelope is |w| + E_m (reading #17)
+    return w - v, v, e_m, np.abs(w) + e_m
 
 
 def dp_step(kinds: list, hp: HParams, t: int, w: list, g_ranks: list, m: list) -> StepResult:

@@ -48,7 +48,10 @@ def hp_kwargs(**kw):
 
 
 def oracle_hp(kw) -> O.HParams:
-    return O.HParams(**{k: v for k, v in kw.items() if k not in ("grad_dtype", "nranks", "tile_elems")})
+    import dataclasses
+
+    names = {f.name for f in dataclasses.fields(O.HParams)}
+    return O.HParams(**{k: v for k, v in kw.items() if k in names})
 
 
 def gate(name: str, got, want, env, tol: float) -> float:

@@ -73,9 +73,13 @@ def main():
         res = {"name": name, "dtype": dtype, "t": t}
         same = all_same(w)  # collectives first: every rank calls them before any rank-local assertion
         red_t, b, e = h.reduced_grad()
+        if red_t.dtype == torch.int16:  # bf16 bit patterns travel as fp16 words (bit-preserving)
+            red_t = red_t.view(torch.float16)
         parts = [torch.empty_like(red_t) for _ in range(P)]
         dist.all_gather(parts, red_t.clone())
         full_red = from_dev(torch.cat(parts))  # the exact buffer every K1 read, all shards
+        if dtype == "bf16":
+            full_red = full_red.view(np.uint16)
         assert torch.equal(g.view(torch.int16) if g.element_size() == 2 else g.view(torch.int32),
                            g_before.view(torch.int16) if g.element_size() == 2 else g_before.view(torch.int32)), \
             "dp step modified the caller's gradient"
