@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--layout", default="resnet50")
+    ap.add_argument("--no-carry", action="store_true",
+                    help="disable LARS_FLAG_CARRY_WNORM (K2 carries sum(w^2) so K1 reads only g)")
     return ap.parse_args()
 
 
@@ -132,8 +134,10 @@ def run_ours(args):
     dtype = "f32" if P == 1 else "f16"
     lay = LY.by_name(args.layout)
     E = sum(t.numel for t in lay)
-    h = PK.Lars([(t.numel, t.kind) for t in lay], device=local, grad_dtype=dtype, nranks=P,
-                grad_scale=1.0 / (G.GRAD_PRESCALE * P), **HP)
+    carry = not args.no_carry
+    mk = lambda flags: PK.Lars([(t.numel, t.kind) for t in lay], device=local, grad_dtype=dtype, nranks=P,
+                               grad_scale=1.0 / (G.GRAD_PRESCALE * P), flags=flags, **HP)
+    h = mk(PK.lars.FLAG_CARRY_WNORM if carry else 0)
     if P > 1:
         h.comm_init_torch()
     gbytes = 4 if dtype == "f32" else 2
@@ -196,6 +200,27 @@ def run_ours(args):
     h.profile_enable(False)
     ph = {kk: max_over_ranks(v / max(1, nsteps)) for kk, v in phases.items()}
 
+    # the same loop without carried weight norms (K1 re-reads w every step), for comparison
+    alt = None
+    if carry:
+        h0 = mk(0)
+        if P > 1:
+            h0.comm_init_torch()
+        step0 = h0.lars_step if P == 1 else h0.dp_allreduce_lars_step
+        for i in range(args.warmup):
+            step0(w, g, m, (T0 + i) % T, stream)
+        barrier()
+        torch.cuda.synchronize()
+        e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e4.record(stream)
+        for i in range(args.steps):
+            step0(w, g, m, (T0 + i) % T, stream)
+        e5.record(stream)
+        torch.cuda.synchronize()
+        alt = max_over_ranks(e4.elapsed_time(e5)) / args.steps
+        h0.close()
+        h.invalidate_carried_norms()  # w was advanced by another handle
+
     # end to end through the public API with host gradients
     g_pin = torch.from_numpy(G.pack(g_host, h.offsets, h.padded_numel)).pin_memory()
     step_h = h.lars_step_host_grad if P == 1 else h.dp_allreduce_lars_step_host_grad
@@ -250,6 +275,7 @@ def run_ours(args):
         "metric": METRIC, "value": round(value, 1), "unit": "params/s", "n_gpus": P, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "grad_dtype": dtype, "data": "synthetic",
+        "carry_wnorm": carry, "no_carry_ms_per_step": None if alt is None else round(alt, 5),
         "config": {"workload": workload_name(P, args.layout), "layout": args.layout, "tensors": len(lay),
                    "params": E, "global_batch": HP["global_batch"], "iters": f"t=({T0}+k) mod {T}",
                    "parallelism": f"dp{P}", "units": f"{P} x {E} gradient params combined+applied per step",

@@ -99,8 +99,14 @@ typedef struct {
   int32_t nranks;        /* data-parallel world size P the layout is planned for (default 1)       */
   int32_t tile_elems;    /* minimum work-tile size in elements; 0 = library default                */
   int32_t shard_policy;  /* lars_shard_policy_t (default LARS_SHARD_CONTIGUOUS)                    */
-  int32_t reserved;      /* must be 0                                                             */
+  uint32_t flags;        /* LARS_FLAG_* (default 0)                                               */
 } lars_hparams_t;
+
+/* Carry the weight norms: K2 also produces sum(w_new^2) for every layer, so the next step's K1 reads only
+ * g (8 -> 4 B/param of norm traffic with fp32 g, 6 -> 2 with fp16). Valid as long as the weights are
+ * changed by this handle's steps only: passing a different w pointer invalidates automatically; call
+ * lars_invalidate_carried_norms after modifying w in place any other way (e.g. loading a checkpoint). */
+#define LARS_FLAG_CARRY_WNORM 1u
 
 typedef struct lars_ctx* lars_handle_t;
 
@@ -198,6 +204,9 @@ lars_status_t lars_reduced_grad(lars_handle_t h, const void** dev_ptr, int64_t* 
  * left untouched). w_norm = ||w_l||, g_norm = ||G_l|| (grad_scale applied), lambda = trust ratio,
  * coef = lr*lambda as the update kernel used it. Any output may be NULL. */
 lars_status_t lars_last_norms(lars_handle_t h, double* w_norm, double* g_norm, double* lambda, double* coef);
+/* Forget the carried weight norms (LARS_FLAG_CARRY_WNORM): the next step recomputes ||w|| from w. */
+lars_status_t lars_invalidate_carried_norms(lars_handle_t h);
+
 /* *skipped: 0 = applied, 1 = skipped (non-finite norm), 2 = skipped (device iteration out of range). */
 lars_status_t lars_last_step_skipped(lars_handle_t h, int32_t* skipped);
 

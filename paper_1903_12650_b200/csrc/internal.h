@@ -16,17 +16,20 @@ constexpr int kThreads = 256;           // threads per CTA of K1 / K2
 #ifndef LARS_NORM_CTAS_PER_SM
 #define LARS_NORM_CTAS_PER_SM 4
 #endif
-#ifndef LARS_UPDATE_CTAS_PER_SM
-#define LARS_UPDATE_CTAS_PER_SM 4
-#endif
 #ifndef LARS_NORM_UNROLL
 #define LARS_NORM_UNROLL 2
 #endif
 constexpr int kCtasPerSm = LARS_NORM_CTAS_PER_SM;      // K1 resident CTAs per SM (one static tile each)
-constexpr int kUpdCtasPerSm = LARS_UPDATE_CTAS_PER_SM; // K2 resident CTAs per SM (dynamic items)
-constexpr int kTilesPerCta = 1;         // tiles per persistent CTA (static round robin)
+#ifndef LARS_NORM_TILES_PER_CTA
+#define LARS_NORM_TILES_PER_CTA 1
+#endif
+#ifndef LARS_NORM_DYNAMIC
+#define LARS_NORM_DYNAMIC 0
+#endif
+constexpr int kTilesPerCta = LARS_NORM_TILES_PER_CTA;  // K1 tiles per persistent CTA
+constexpr bool kNormDynamic = LARS_NORM_DYNAMIC != 0;  // K1 tiles from a ticket counter
 constexpr int32_t kMaxTileChunks = 256; // chunk partials of one tile live in shared memory
-constexpr int32_t kUpdateSplit = 4;     // K2 work items per tile (dynamically scheduled)
+constexpr int32_t kUpdateSplit = 4;     // K2 walks each tile in 4 parts, last part first
 constexpr int kNormUnroll = LARS_NORM_UNROLL;  // K1 vector groups per lane per iteration
 constexpr int32_t kDefaultMinTile = 4096;
 constexpr int32_t kChunk = 2048;        // elements per warp work item (multiple of 256)
@@ -98,16 +101,17 @@ struct DevWork {
   int32_t nsplit_total;         // split layers in the whole plan (C3 payload: 1 + 2 * nsplit_total doubles)
   int32_t ntiles;
   int32_t ntensors;
-  int32_t grid;      // K1 CTAs: one per tile
-  int32_t upd_grid;  // K2 persistent CTAs: min(ntiles * kUpdateSplit, SMs * kUpdCtasPerSm)
+  int32_t grid;      // K1 and K2 CTAs (same grid: CTA b runs on the same SM in both kernels)
 };
 
 struct DevScratch {
-  // Tile tickets of K1 ([0]) and K2 ([1]): monotonically increasing, never reset. A launch performs
-  // exactly ntiles + grid fetches (one failing fetch per CTA), so ticket % (ntiles + grid) is the
-  // tile index within the launch — CUDA-graph safe, no per-step memset.
+  // Tile tickets of K1 ([0], kNormDynamic only; [1] spare): monotonically increasing, never reset. A
+  // launch performs exactly ntiles + grid fetches (one failing fetch per CTA), so ticket % (ntiles + grid)
+  // is the tile index within the launch — CUDA-graph safe, no per-step memset.
   unsigned long long* ticket;
   double* cpart_w;       // per chunk: sum w^2 of the chunk
+  double* cpart_wnext;   // per chunk: sum w_new^2 written by K2 in carry mode (LARS_FLAG_CARRY_WNORM)
+  int32_t* wnext_valid;  // 1 when cpart_wnext describes the current w (set by K2, cleared by the host)
   double* cpart_g;       // per chunk: sum g^2
   double* part_w;        // per segment: sum w^2 of the segment
   double* part_g;        // per segment: sum g^2
@@ -133,6 +137,7 @@ struct Hyper {
   int64_t total_iters;       // T (device-side range check for iter_dev)
   double eta, weight_decay, eps, grad_scale;
   float mu, grad_scale_f;
+  bool carry;                // LARS_FLAG_CARRY_WNORM
 };
 
 // g_shift: the gradient of flat element e is g[e - g_shift] (the DP step reads its reduced shard).

@@ -195,7 +195,7 @@ template <int DT>
 __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, const DevScratch& sc, const Hyper& hy,
                                            const float* __restrict__ w, const void* __restrict__ g,
                                            int64_t g_shift, double* sm_cw, double* sm_cg, unsigned* sm_done,
-                                           unsigned* sm_nonfinite) {
+                                           unsigned* sm_nonfinite, bool carried) {
   constexpr int kWarps = kThreads / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // Phase A: the warps of the CTA stream the tile's chunks independently (no block barrier per layer);
@@ -206,6 +206,32 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
     const float* wp = w + ck.begin;
     const int64_t gi = ck.begin - g_shift;
     const int32_t ng = ck.len >> 3;
+    if (carried) {  // sum(w^2) of this chunk was produced by the previous K2: stream g only
+      double ag = 0.0, ag1 = 0.0;
+      int32_t j = lane;
+      for (; j + 96 < ng; j += 128) {  // 4 x 32 B in flight per lane
+        F8 gv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) gv[u] = Grad<DT>::load8_keep(g, gi + 8 * (j + 32 * u));
+        acc8(ag, gv[0]);
+        acc8(ag1, gv[1]);
+        acc8(ag, gv[2]);
+        acc8(ag1, gv[3]);
+      }
+      for (; j < ng; j += 32) acc8(ag, Grad<DT>::load8_keep(g, gi + 8 * j));
+      ag += ag1;
+      for (int32_t i = (ng << 3) + lane; i < ck.len; i += 32) {
+        const double y = (double)Grad<DT>::load1(g, gi + i);
+        ag = fma(y, y, ag);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ag += __shfl_xor_sync(0xffffffffu, ag, o);
+      if (lane == 0) {
+        sm_cw[c - c0] = __ldcg(sc.cpart_wnext + c);
+        sm_cg[c - c0] = ag;
+      }
+      continue;
+    }
     double aw = 0.0, ag = 0.0, aw1 = 0.0, ag1 = 0.0;
     int32_t j = lane;
     for (; j + (kNormUnroll - 1) * 32 < ng; j += kNormUnroll * 32) {
@@ -315,8 +341,14 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
   }
 }
 
-// K1. Static persistent schedule: CTA b owns tiles b, b + grid, ...
-template <int DT>
+// Ticket counters are monotonic (never reset): one launch draws exactly nitems + grid tickets (one
+// failing draw per CTA), so ticket % (nitems + grid) is the item index within the launch.
+__device__ __forceinline__ int32_t take_ticket(unsigned long long* t, int32_t nitems, int32_t grid) {
+  return (int32_t)(atomicAdd(t, 1ull) % (unsigned long long)(nitems + grid));
+}
+
+// K1. Persistent schedule: static (CTA b owns tiles b, b + grid, ...) or dynamic (kNormDynamic).
+template <int DT, bool CARRY>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_norms_kernel(DevWork wk, DevScratch sc, Hyper hy,
                                                                           const float* __restrict__ w,
                                                                           const void* __restrict__ g,
@@ -330,9 +362,28 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_norms_kernel(DevWor
   }
   pdl_wait();
   TRACE_BEGIN
-  for (int32_t tile = blockIdx.x; tile < wk.ntiles; tile += gridDim.x) {
-    __syncthreads();  // shared chunk partials of the previous tile fully consumed
-    norms_tile<DT>(tile, wk, sc, hy, w, g, g_shift, sm_cw, sm_cg, &sm_done, &sm_nonfinite);
+  // carry mode: the previous K2 left sum(w_new^2) per chunk; valid until the host invalidates it
+  const bool carried = CARRY && *(volatile const int32_t*)sc.wnext_valid != 0;
+  if (kNormDynamic) {  // tiles handed out by a ticket counter (faster CTAs take more tiles)
+    __shared__ int32_t s_tile;
+    if (threadIdx.x == 0) s_tile = take_ticket(sc.ticket + 0, wk.ntiles, gridDim.x);
+    __syncthreads();
+    int32_t tile = s_tile;
+    while (tile < wk.ntiles) {
+      __syncthreads();  // s_tile read by all; shared chunk partials of the previous tile consumed
+      int32_t next = 0;
+      if (threadIdx.x == 0) next = take_ticket(sc.ticket + 0, wk.ntiles, gridDim.x);
+      norms_tile<DT>(tile, wk, sc, hy, w, g, g_shift, sm_cw, sm_cg, &sm_done, &sm_nonfinite, carried);
+      __syncthreads();
+      if (threadIdx.x == 0) s_tile = next;
+      __syncthreads();
+      tile = s_tile;
+    }
+  } else {
+    for (int32_t tile = blockIdx.x; tile < wk.ntiles; tile += gridDim.x) {
+      __syncthreads();  // shared chunk partials of the previous tile fully consumed
+      norms_tile<DT>(tile, wk, sc, hy, w, g, g_shift, sm_cw, sm_cg, &sm_done, &sm_nonfinite, carried);
+    }
   }
   __syncthreads();
   TRACE_END(0)
@@ -371,7 +422,9 @@ __device__ __forceinline__ void upd8(F8& w, F8& m, const F8& g, float s, float c
   }
 }
 
-template <int DT>
+__device__ __forceinline__ void accw8(double& a, const F8& x) { acc8(a, x); }
+
+template <int DT, bool CARRY>
 __device__ __forceinline__ void update_item(int32_t item, const DevWork& wk, const DevScratch& sc, const Hyper& hy,
                                             float* __restrict__ w, const void* __restrict__ g, int64_t g_shift,
                                             float* __restrict__ m) {
@@ -391,12 +444,14 @@ __device__ __forceinline__ void update_item(int32_t item, const DevWork& wk, con
     float* mp = m + ck.begin;
     const int64_t gi = ck.begin - g_shift;
     const int32_t ng = ck.len >> 3;
+    double aw = 0.0, aw1 = 0.0;  // CARRY: sum(w_new^2) of this chunk for the next step's K1
     for (int32_t i = (ng << 3) + lane; i < ck.len; i += 32) {  // ragged tensor tail (< 8 elements)
       const float wv = wp[i], mv = mp[i];
       const float u = fmaf(b, wv, s * Grad<DT>::load1(g, gi + i));
       const float v = fmaf(mu, mv, cf * u);
       wp[i] = wv - v;
       mp[i] = v;
+      if (CARRY) aw = fma((double)(wv - v), (double)(wv - v), aw);
     }
     int32_t j = ng - 1 - lane;
     for (; j - 32 >= 0; j -= 64) {
@@ -410,6 +465,10 @@ __device__ __forceinline__ void update_item(int32_t item, const DevWork& wk, con
       st8(mp + 8 * j, m0);
       st8(wp + 8 * j1, w1);
       st8(mp + 8 * j1, m1);
+      if (CARRY) {
+        accw8(aw, w0);
+        accw8(aw1, w1);
+      }
     }
     if (j >= 0) {
       F8 w0 = ld8_rw(wp + 8 * j), m0 = ld8_rw(mp + 8 * j);
@@ -417,41 +476,36 @@ __device__ __forceinline__ void update_item(int32_t item, const DevWork& wk, con
       upd8(w0, m0, g0, s, cf, b, mu);
       st8(wp + 8 * j, w0);
       st8(mp + 8 * j, m0);
+      if (CARRY) accw8(aw, w0);
+    }
+    if (CARRY) {
+      aw += aw1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) aw += __shfl_xor_sync(0xffffffffu, aw, o);
+      if (lane == 0) sc.cpart_wnext[c] = aw;
     }
   }
 }
 
-// K2. Dynamic persistent schedule: ntiles * kUpdateSplit items handed out by a ticket counter, so a
-// CTA that gets less memory bandwidth simply takes fewer items (per-CTA bandwidth on a loaded B200
-// varies by ~1.5x; a static split would wait for the slowest CTA).
-__device__ __forceinline__ int32_t take_ticket(unsigned long long* t, int32_t nitems, int32_t grid) {
-  return (int32_t)(atomicAdd(t, 1ull) % (unsigned long long)(nitems + grid));
-}
-
-template <int DT>
-__global__ void __launch_bounds__(kThreads, kUpdCtasPerSm) lars_update_kernel(DevWork wk, DevScratch sc, Hyper hy,
+// K2. Same persistent schedule as K1 (CTA b owns tiles b, b + grid, ...; identical grid and resources,
+// so CTA b runs on the same SM in both kernels) and each tile's chunks walked backwards: the gradient
+// bytes K1 streamed last into this SM's L2 slice are re-read first.
+template <int DT, bool CARRY>
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_update_kernel(DevWork wk, DevScratch sc, Hyper hy,
                                                                            float* __restrict__ w,
                                                                            const void* __restrict__ g,
                                                                            int64_t g_shift, float* __restrict__ m) {
-  __shared__ int32_t s_item;
   pdl_trigger();
   pdl_wait();
-  // A skipped step still draws its tickets, keeping the ticket arithmetic of the next launch aligned.
   const bool skip = *(volatile const int32_t*)sc.skip != 0;  // whole step skipped (non-finite norm)
-  const int32_t nitems = wk.ntiles * kUpdateSplit;
   TRACE_BEGIN
-  if (threadIdx.x == 0) s_item = take_ticket(sc.ticket + 1, nitems, gridDim.x);
-  __syncthreads();
-  int32_t item = s_item;
-  while (item < nitems) {
-    __syncthreads();  // everyone has read s_item
-    int32_t next = 0;
-    if (threadIdx.x == 0) next = take_ticket(sc.ticket + 1, nitems, gridDim.x);  // consumed one item later
-    if (!skip) update_item<DT>(item, wk, sc, hy, w, g, g_shift, m);
-    if (threadIdx.x == 0) s_item = next;
-    __syncthreads();
-    item = s_item;
-  }
+  if (!skip)
+    for (int32_t tile = blockIdx.x; tile < wk.ntiles; tile += gridDim.x)
+      for (int32_t q = kUpdateSplit - 1; q >= 0; --q)
+        update_item<DT, CARRY>((kUpdateSplit - 1 - q) * wk.ntiles + tile, wk, sc, hy, w, g, g_shift, m);
+  // every chunk's sum(w_new^2) is written once this grid completes; the next K1 (stream-ordered after
+  // the whole grid) may use them. A skipped step leaves w — and therefore the old sums — valid.
+  if (CARRY && !skip && blockIdx.x == 0 && threadIdx.x == 0) *(volatile int32_t*)sc.wnext_valid = 1;
   TRACE_END(1)
 }
 
@@ -515,12 +569,14 @@ static cudaError_t launch_pdl(K kernel, int grid, cudaStream_t stream, Args... a
 template <int DT>
 static cudaError_t launch_norms_t(const DevWork& wk, const DevScratch& sc, const Hyper& hy, const float* w,
                                   const void* g, int64_t g_shift, cudaStream_t st) {
-  return launch_pdl(lars_norms_kernel<DT>, wk.grid, st, wk, sc, hy, w, g, g_shift);
+  if (hy.carry) return launch_pdl(lars_norms_kernel<DT, true>, wk.grid, st, wk, sc, hy, w, g, g_shift);
+  return launch_pdl(lars_norms_kernel<DT, false>, wk.grid, st, wk, sc, hy, w, g, g_shift);
 }
 template <int DT>
 static cudaError_t launch_update_t(const DevWork& wk, const DevScratch& sc, const Hyper& hy, float* w,
                                    const void* g, int64_t g_shift, float* m, cudaStream_t st) {
-  return launch_pdl(lars_update_kernel<DT>, wk.upd_grid, st, wk, sc, hy, w, g, g_shift, m);
+  if (hy.carry) return launch_pdl(lars_update_kernel<DT, true>, wk.grid, st, wk, sc, hy, w, g, g_shift, m);
+  return launch_pdl(lars_update_kernel<DT, false>, wk.grid, st, wk, sc, hy, w, g, g_shift, m);
 }
 
 cudaError_t launch_norms(int32_t dt, const DevWork& wk, const DevScratch& sc, const Hyper& hy, const float* w,

@@ -31,6 +31,7 @@ struct DevBufs {
   DevWork dw{};
   DevScratch sc{};
   void* mem = nullptr;
+  const float* carry_w = nullptr;  // weights the carried norms describe (carry mode)
 };
 
 size_t dtype_size(int32_t dt) { return dt == LARS_F32 ? 4 : 2; }
@@ -62,6 +63,7 @@ lars_status_t upload(DevBufs& b, int sms, int32_t nsplit_total, bool dp) {
   auto add = [&](size_t n, size_t sz) { bytes += (n * sz + 255) / 256 * 256; };
   add(ns, sizeof(Seg)); add(ntl, 4); add(nt, 4); add(nt, 4); add(nt, 4);                // work list
   add(nc, sizeof(Seg)); add(ntl, 4); add(ns + 1, 4); add(nc, 8); add(nc, 8);            // chunks
+  add(nc, 8); add(1, 4);                                                                // carried norms
   add(2, 8);                                                                            // tickets
   add(nt, 4); add(nt, 4); add(dp ? 1 + 2 * (size_t)nsplit_total : 1, 8);                // split layers, C3
   add(ns, 8); add(ns, 8); add(nt, 4); add(1, 4); add(1, 4); add(1, 4);                  // partials, counters
@@ -86,6 +88,8 @@ lars_status_t upload(DevBufs& b, int sms, int32_t nsplit_total, bool dp) {
   for (size_t i = 0; i < wl.tsplit.size(); ++i)
     if (wl.tsplit[i] >= 0) locals.push_back((int32_t)i);
   b.sc.cpart_w = carve<double>(p, nc);
+  b.sc.cpart_wnext = carve<double>(p, nc);
+  b.sc.wnext_valid = carve<int32_t>(p, 1);
   b.sc.cpart_g = carve<double>(p, nc);
   b.sc.part_w = carve<double>(p, ns);
   b.sc.part_g = carve<double>(p, ns);
@@ -108,8 +112,7 @@ lars_status_t upload(DevBufs& b, int sms, int32_t nsplit_total, bool dp) {
     return LARS_ERR_CUDA;
   b.dw = DevWork{segs, tile_seg, chunks, tile_chunk, seg_chunk, tsb, tsc, tl, tsplit, split_locals,
                  (int32_t)locals.size(), dp ? nsplit_total : 0, wl.ntiles(), (int32_t)wl.tensors.size(),
-                 std::min<int32_t>(wl.ntiles(), sms * kCtasPerSm),
-                 std::min<int32_t>(wl.ntiles() * kUpdateSplit, sms * kUpdCtasPerSm)};
+                 std::min<int32_t>(wl.ntiles(), sms * kCtasPerSm)};
   (void)sms;
   return LARS_OK;
 }
@@ -298,12 +301,25 @@ static lars_status_t check_step_args(lars_handle_t h, const void* w, const void*
 
 static Hyper hyper(lars_handle_t h, int64_t iter, int64_t* iter_dev = nullptr) {
   return Hyper{h->lr_d, iter, iter_dev, h->plan.T, h->hp.eta, h->hp.weight_decay, h->hp.eps, h->hp.grad_scale,
-               (float)h->hp.momentum, (float)h->hp.grad_scale};
+               (float)h->hp.momentum, (float)h->hp.grad_scale, (h->hp.flags & LARS_FLAG_CARRY_WNORM) != 0};
+}
+
+// Carry mode: the norms K2 left are only valid for the weights it wrote. A different weight buffer (or
+// an explicit lars_invalidate_carried_norms) makes the next K1 recompute ||w|| from w.
+static lars_status_t carry_guard(lars_handle_t h, DevBufs& b, const float* w, cudaStream_t s) {
+  if (!(h->hp.flags & LARS_FLAG_CARRY_WNORM)) return LARS_OK;
+  if (b.carry_w != w) {
+    CUDA_OR(cudaMemsetAsync(b.sc.wnext_valid, 0, sizeof(int32_t), s));
+    b.carry_w = w;
+  }
+  return LARS_OK;
 }
 
 static lars_status_t step_impl(lars_handle_t h, float* w, const void* g, float* m, const Hyper& hy, void* stream) {
   DeviceGuard dg(h->device);
   cudaStream_t s = (cudaStream_t)stream;
+  lars_status_t cg = carry_guard(h, h->full, w, s);
+  if (cg != LARS_OK) return cg;
   auto* pe = h->prof.begin(1);
   prof_rec(pe, 0, s);
   CUDA_OR(launch_norms(h->hp.grad_dtype, h->full.dw, h->full.sc, hy, w, g, 0, s));       // K1
@@ -395,6 +411,8 @@ static lars_status_t dp_impl(lars_handle_t h, float* w, const void* g, float* m,
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t S = h->plan.S, begin = (int64_t)h->rank * S;
   const int32_t dt = h->hp.grad_dtype;
+  lars_status_t cg = carry_guard(h, h->shard, w, s);
+  if (cg != LARS_OK) return cg;
   auto* pe = h->prof.begin(2);
   prof_rec(pe, 0, s);
   NCCL_OR(ncclReduceScatter(g, h->gred, (size_t)S, nccl_type(dt), ncclSum, h->comm, s));          // C1
@@ -537,6 +555,13 @@ lars_status_t lars_last_norms(lars_handle_t h, double* w_norm, double* g_norm, d
     if (lambda) lambda[l] = la[i];
     if (coef) coef[l] = (double)cf[i];
   }
+  return LARS_OK;
+}
+
+lars_status_t lars_invalidate_carried_norms(lars_handle_t h) {
+  if (!h) return LARS_ERR_INVALID_ARG;
+  h->full.carry_w = nullptr;
+  h->shard.carry_w = nullptr;
   return LARS_OK;
 }
 

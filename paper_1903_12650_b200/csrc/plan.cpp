@@ -165,7 +165,13 @@ static WorkList make_worklist_once(const Plan& p, int32_t rank, int32_t ntiles_t
 // Tiles are balanced by COST, not elements: a piece of a layer costs its elements plus a fixed
 // latency-equivalent per warp chunk and per segment (a 64-element BN vector still costs a memory round
 // trip and a per-layer finish), so tiles full of small layers hold fewer elements.
-constexpr int64_t kChunkCost = 384, kSegCost = 512;
+#ifndef LARS_CHUNK_COST
+#define LARS_CHUNK_COST 384
+#endif
+#ifndef LARS_SEG_COST
+#define LARS_SEG_COST 512
+#endif
+constexpr int64_t kChunkCost = LARS_CHUNK_COST, kSegCost = LARS_SEG_COST;
 
 WorkList make_worklist(const Plan& p, int32_t rank, int32_t ntiles_target, int32_t min_tile) {
   int64_t cost = 0;

@@ -23,6 +23,7 @@ KIND = {"weight": 0, "bias": 1, "bn_gamma": 2, "bn_beta": 3}
 DTYPE = {"f32": 0, "f16": 1, "bf16": 2}
 DTYPE_BYTES = {"f32": 4, "f16": 2, "bf16": 2}
 SHARD_POLICY = {"contiguous": 0, "lpt": 1}
+FLAG_CARRY_WNORM = 1
 
 
 class LarsLibraryMissing(RuntimeError):
@@ -44,7 +45,7 @@ class HParams(ctypes.Structure):
                 ("eps", c_double), ("warmup_epochs", c_double), ("poly_power", c_double),
                 ("grad_scale", c_double), ("global_batch", c_int64), ("dataset_size", c_int64),
                 ("total_epochs", c_int32), ("grad_dtype", c_int32), ("nranks", c_int32),
-                ("tile_elems", c_int32), ("shard_policy", c_int32), ("reserved", c_int32)]
+                ("tile_elems", c_int32), ("shard_policy", c_int32), ("flags", ctypes.c_uint32)]
 
 
 _lib = None
@@ -82,6 +83,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "lars_last_norms": (c_int32, [h, POINTER(c_double), POINTER(c_double), POINTER(c_double),
                                       POINTER(c_double)]),
         "lars_last_step_skipped": (c_int32, [h, POINTER(c_int32)]),
+        "lars_invalidate_carried_norms": (c_int32, [h]),
         "lars_destroy": (c_int32, [h]),
         "lars_strerror": (ctypes.c_char_p, [c_int32]),
         "lars_version": (ctypes.c_char_p, []),
@@ -278,6 +280,9 @@ class Lars:
         a, b, c, d = [(c_double * self.n)(*([float("nan")] * self.n)) for _ in range(4)]
         _check(self._lib.lars_last_norms(self._h, a, b, c, d), "lars_last_norms")
         return list(a), list(b), list(c), list(d)
+
+    def invalidate_carried_norms(self) -> None:
+        _check(self._lib.lars_invalidate_carried_norms(self._h), "lars_invalidate_carried_norms")
 
     def last_step_status(self) -> int:
         """0 applied, 1 skipped (non-finite norm), 2 skipped (device iteration out of range)."""

@@ -217,3 +217,50 @@ def test_device_argument_errors():
         s.h.comm_init(0, 2, bytes(128))
     assert e.value.status == 8  # planned for nranks = 1
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f16"])
+def test_carried_weight_norms_chain(dtype):
+    """LARS_FLAG_CARRY_WNORM: K2 leaves sum(w_new^2) per chunk, the next K1 reads only g. Each step of a
+    5-step chain (first step recomputes, the rest carry) is checked against the oracle from the GPU's
+    pre-step state, and against a non-carry handle fed the same inputs."""
+    torch = _torch()
+    lay = LY.resnet50()[:70] + LY.random_layout(np.random.default_rng(21), 15)
+    a = GpuStep(lay, grad_dtype=dtype, flags=1)
+    b = GpuStep(lay, grad_dtype=dtype)
+    w, m = G.weights(lay), G.momentum(lay, 1e-3)
+    a.upload(w, G.grads(lay, 0, 0, dtype), m)
+    b.upload(w, G.grads(lay, 0, 0, dtype), m)
+    for t in range(300, 305):
+        g = G.grads(lay, 0, t, dtype)
+        a.g = to_dev(G.pack(g, a.h.offsets, a.h.padded_numel))
+        b.g = to_dev(G.pack(g, b.h.offsets, b.h.padded_numel))
+        pre_w, pre_m = a.state()
+        a.step(t)
+        b.step(t)
+        a.check(t, pre_w, [g], pre_m, TOL_F32, tag=f"carry {dtype} t={t}")
+        wa, na = a.h.last_norms()[0], None
+        wb = b.h.last_norms()[0]
+        assert np.allclose(wa, wb, rtol=1e-13, atol=0)
+    torch.cuda.synchronize()
+
+
+def test_carried_norms_invalidation():
+    torch = _torch()
+    lay = LY.tiny()
+    s = GpuStep(lay, flags=1)
+    w, g, m = G.weights(lay), G.grads(lay, 0, 1, "f32"), G.momentum(lay, 1e-3)
+    s.upload(w, g, m)
+    s.step(100)
+    s.step(101)
+    with torch.no_grad():
+        s.w.mul_(2.0)  # modified in place behind the library's back
+    s.h.invalidate_carried_norms()
+    pre_w, pre_m = s.state()
+    s.step(102)
+    s.check(102, pre_w, [g], pre_m, TOL_F32, tag="after invalidate")
+    # a different weight buffer invalidates automatically
+    s.w = s.w.clone() * 0.5
+    pre_w, pre_m = s.state()
+    s.step(103)
+    s.check(103, pre_w, [g], pre_m, TOL_F32, tag="new w buffer")

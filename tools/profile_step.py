@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--flags", type=int, default=0, help="lars_hparams_t.flags (1 = carry weight norms)")
     a = ap.parse_args()
     import torch
 
@@ -28,7 +29,7 @@ def main():
 
     lay = LY.by_name(a.layout)
     h = PK.Lars([(t.numel, t.kind) for t in lay], device=0, grad_dtype=a.dtype, base_lr=32.0,
-                grad_scale=1.0 / G.GRAD_PRESCALE)
+                grad_scale=1.0 / G.GRAD_PRESCALE, flags=a.flags)
     dev = torch.device("cuda", 0)
     w = torch.from_numpy(G.pack(G.weights(lay), h.offsets, h.padded_numel)).to(dev)
     g = torch.from_numpy(G.pack(G.grads(lay, 0, 0, a.dtype), h.offsets, h.padded_numel)).to(dev)

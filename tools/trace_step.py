@@ -21,7 +21,8 @@ def main():
     layout = sys.argv[1] if len(sys.argv) > 1 else "resnet50"
     dtype = sys.argv[2] if len(sys.argv) > 2 else "f32"
     lay = LY.by_name(layout)
-    h = PK.Lars([(t.numel, t.kind) for t in lay], device=0, grad_dtype=dtype, base_lr=32.0, grad_scale=1 / 1024)
+    h = PK.Lars([(t.numel, t.kind) for t in lay], device=0, grad_dtype=dtype, base_lr=32.0, grad_scale=1 / 1024,
+                flags=int(os.environ.get("TRACE_FLAGS", "0")))
     dev = torch.device("cuda", 0)
     w = torch.from_numpy(G.pack(G.weights(lay), h.offsets, h.padded_numel)).to(dev)
     g = torch.from_numpy(G.pack(G.grads(lay, 0, 0, dtype), h.offsets, h.padded_numel)).to(dev)
