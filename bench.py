@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--layout", default="resnet50")
+    ap.add_argument("--no-fused", action="store_true",
+                    help="P > 1: use the NCCL collective path instead of the fused NVLink kernels")
     ap.add_argument("--no-carry", action="store_true",
                     help="disable LARS_FLAG_CARRY_WNORM (K2 carries sum(w^2) so K1 reads only g)")
     return ap.parse_args()
@@ -148,6 +150,15 @@ def run_ours(args):
 
     w_host, g_host, m_host = G.weights(lay), G.grads(lay, rank, 0, dtype), G.momentum(lay, 1e-3)
     w, g, m = dev_flat(w_host), dev_flat(g_host), dev_flat(m_host)
+    w_n, g_n, fused = w, g, False
+    if P > 1 and not args.no_fused:  # library-owned symmetric buffers -> fused NVLink path
+        try:
+            w_s, g_s = h.dp_buffers()
+            w_s.copy_(w)
+            g_s.copy_(g)
+            w, g, fused = w_s, g_s, True
+        except PK.LarsError:
+            pass
     T = h.total_iters
     step = h.lars_step if P == 1 else h.dp_allreduce_lars_step
     stream = torch.cuda.current_stream()
@@ -200,29 +211,33 @@ def run_ours(args):
     h.profile_enable(False)
     ph = {kk: max_over_ranks(v / max(1, nsteps)) for kk, v in phases.items()}
 
-    # the same loop without carried weight norms (K1 re-reads w every step), for comparison
-    alt = None
-    if carry:
-        h0 = mk(0)
-        if P > 1:
-            h0.comm_init_torch()
-        step0 = h0.lars_step if P == 1 else h0.dp_allreduce_lars_step
+    # comparison loops: P = 1 without carried weight norms (K1 re-reads w every step); P > 1 the NCCL
+    # collective path (reduce-scatter + K1 + allreduce + K2 + all-gather) on ordinary buffers
+    alt = {}
+
+    def time_loop(fn, ww, gg):
         for i in range(args.warmup):
-            step0(w, g, m, (T0 + i) % T, stream)
+            fn(ww, gg, m, (T0 + i) % T, stream)
         barrier()
         torch.cuda.synchronize()
         e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e4.record(stream)
         for i in range(args.steps):
-            step0(w, g, m, (T0 + i) % T, stream)
+            fn(ww, gg, m, (T0 + i) % T, stream)
         e5.record(stream)
         torch.cuda.synchronize()
-        alt = max_over_ranks(e4.elapsed_time(e5)) / args.steps
+        return round(max_over_ranks(e4.elapsed_time(e5)) / args.steps, 5)
+
+    if P == 1 and carry:
+        h0 = mk(0)
+        alt["no_carry_ms_per_step"] = time_loop(h0.lars_step, w, g)
         h0.close()
         h.invalidate_carried_norms()  # w was advanced by another handle
+    if P > 1 and fused:
+        alt["nccl_path_ms_per_step"] = time_loop(h.dp_allreduce_lars_step, w_n, g_n)
 
     # end to end through the public API with host gradients
-    g_pin = torch.from_numpy(G.pack(g_host, h.offsets, h.padded_numel)).pin_memory()
+    g_pin = torch.from_numpy(G.pack(g_host, h.offsets, h.padded_numel)).pin_memory()  # lands in g's buffer
     step_h = h.lars_step_host_grad if P == 1 else h.dp_allreduce_lars_step_host_grad
     ne = max(1, args.e2e_steps)
     step_h(w, g_pin, m, T0 % T, stream)
@@ -264,9 +279,14 @@ def run_ours(args):
                 "peak_source": peak_note}
     else:
         bus = (P - 1) / P * (gbytes + 4) * h.padded_numel
-        coll_ms = ph["reduce_scatter"] + ph["all_gather"]
+        if fused:  # F1 (reduce+norms) + FX + F2 (update+gather): the transfers ARE these kernels
+            coll_ms = ph["norms"] + ph["skip_allreduce"] + ph["update"]
+            kname = "fused NVLink path F1 reduce+norms, FX, F2 update+gather"
+        else:
+            coll_ms = ph["reduce_scatter"] + ph["all_gather"]
+            kname = "NCCL reduce-scatter + all-gather (C1+C2)"
         ach = bus / (coll_ms * 1e-3) / 1e9
-        roof = {"bound": "nvlink", "kernel": "NCCL reduce-scatter + all-gather (C1+C2)", "achieved": round(ach, 1),
+        roof = {"bound": "nvlink", "kernel": kname, "achieved": round(ach, 1),
                 "peak": NVLINK_PEER_GBS, "unit": "GB/s", "frac": round(ach / NVLINK_PEER_GBS, 4), "traffic": None,
                 "bus_bytes_per_step": int(bus), "peak_source": "measured peer copy per direction, B200_PROFILING.md",
                 "step_frac_of_bus_roofline": round(bus / NVLINK_PEER_GBS / 1e9 / (ms_step * 1e-3), 4)}
@@ -275,10 +295,11 @@ def run_ours(args):
         "metric": METRIC, "value": round(value, 1), "unit": "params/s", "n_gpus": P, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "grad_dtype": dtype, "data": "synthetic",
-        "carry_wnorm": carry, "no_carry_ms_per_step": None if alt is None else round(alt, 5),
+        "carry_wnorm": carry, **alt,
         "config": {"workload": workload_name(P, args.layout), "layout": args.layout, "tensors": len(lay),
                    "params": E, "global_batch": HP["global_batch"], "iters": f"t=({T0}+k) mod {T}",
                    "parallelism": f"dp{P}", "units": f"{P} x {E} gradient params combined+applied per step",
+                   "dp_path": None if P == 1 else ("fused-nvlink" if fused else "nccl"),
                    "l2": f"inputs larger than L2: w+g+m = {(8 + gbytes) * h.padded_numel / 1e6:.0f} MB > 126 MB, "
                          "no flush"},
         "phases_ms": {kk: round(v, 5) for kk, v in ph.items() if v > 0},
@@ -289,8 +310,8 @@ def run_ours(args):
         "e2e": {"value": round(units / (ms_e2e * 1e-3), 1), "unit": "params/s", "ms_per_step": round(ms_e2e, 4),
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "clocks": clk,
-        "gpu_launches": 2 * args.steps,
-        "nccl_launches": (3 * args.steps) if P > 1 else 0,
+        "gpu_launches": (3 if fused else 2 if P == 1 else 3) * args.steps,
+        "nccl_launches": (3 * args.steps) if (P > 1 and not fused) else 0,
     }
     if P == 1 and rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(lay, w_host, [g_host], m_host, dtype, P)

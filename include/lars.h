@@ -191,14 +191,26 @@ lars_status_t dp_allreduce_lars_step_host_grad(lars_handle_t h, float* w, const 
 /* Per-phase device timing with CUDA events recorded on the step's stream (instrumentation for benchmarks;
  * off by default). lars_profile_enable(h, 1) clears the accumulators and starts recording;
  * lars_profile_enable(h, 0) stops. lars_profile_read synchronizes and returns accumulated milliseconds per
- * phase since enable: ms[0] reduce-scatter (C1), ms[1] norms (K1), ms[2] skip-flag allreduce (C3),
- * ms[3] update (K2), ms[4] all-gather (C2); single-GPU steps fill ms[1] and ms[3]. *steps = steps timed. */
+ * phase since enable: ms[0] reduce-scatter (C1), ms[1] norms (K1), ms[2] skip/split allreduce (C3 +
+ * finisher), ms[3] update (K2), ms[4] all-gather (C2); single-GPU steps fill ms[1] and ms[3]; the fused
+ * data-parallel path fills ms[1] (F1: reduce + norms), ms[2] (FX) and ms[3] (F2: update + gather).
+ * *steps = steps timed. */
 lars_status_t lars_profile_enable(lars_handle_t h, int32_t enable);
 lars_status_t lars_profile_read(lars_handle_t h, double* ms, int64_t* steps);
 
-/* Device pointer to the reduced gradient shard of the last dp step (S elements of grad_dtype, first
- * element = global element `begin` of this rank's shard). Owned by the library. */
-lars_status_t lars_reduced_grad(lars_handle_t h, const void** dev_ptr, int64_t* begin, int64_t* end);
+/* The library-owned weight (fp32) and gradient (grad_dtype) buffers of the FUSED data-parallel path:
+ * padded_numel elements each, in NCCL symmetric memory (ncclMemAlloc + window registration) so every rank
+ * reaches every other rank's buffers over NVLink. When dp_allreduce_lars_step is given exactly these two
+ * pointers it runs three kernels instead of NCCL collectives + two kernels: F1 sums this rank's shard of the
+ * gradient over all ranks (fp32, rank order) while computing the layer norms, FX exchanges the skip flag and
+ * split-layer sums, F2 updates the shard and stores every new weight into every rank's buffer (the
+ * all-gather). Available after lars_comm_init when all ranks share one NVLink domain (NCCL LSA team = world)
+ * and LARS_DP_FUSED is not "0"; otherwise LARS_ERR_NO_COMM. Other pointers keep the NCCL path. */
+lars_status_t lars_dp_buffers(lars_handle_t h, float** w, void** g);
+
+/* Device pointer to the reduced gradient shard of the last dp step (S elements of *dtype: the wire dtype on
+ * the NCCL path, LARS_F32 on the fused path; first element = global element `begin`). Owned by the library. */
+lars_status_t lars_reduced_grad(lars_handle_t h, const void** dev_ptr, int32_t* dtype, int64_t* begin, int64_t* end);
 
 /* Synchronizing readbacks of the last step (per tensor; entries of tensors this rank does not own are
  * left untouched). w_norm = ||w_l||, g_norm = ||G_l|| (grad_scale applied), lambda = trust ratio,

@@ -6,6 +6,9 @@
 #include <vector>
 
 #include <cuda_runtime_api.h>
+#include <nccl.h>
+#include <nccl_device/core.h>
+#include <nccl_device/impl/comm__types.h>
 
 #include "lars.h"
 
@@ -145,6 +148,18 @@ cudaError_t launch_norms(int32_t grad_dtype, const DevWork& wk, const DevScratch
                          const float* w, const void* g, int64_t g_shift, cudaStream_t stream);
 cudaError_t launch_update(int32_t grad_dtype, const DevWork& wk, const DevScratch& sc, const Hyper& hy,
                           float* w, const void* g, int64_t g_shift, float* m, cudaStream_t stream);
+// Device handles of the fused data-parallel path (symmetric NCCL windows + device communicator).
+struct DpFused {
+  ncclDevComm dc;
+  ncclWindow_t gwin, wwin, xwin;  // gradients (wire dtype), weights (fp32), C3 exchange slots (fp64)
+  int rank, nranks;
+  int64_t begin;                  // first element of this rank's shard
+  float* gred;                    // fp32 reduced shard (S elements)
+};
+// F1 (reduce + norms), FX (exchange + finish), F2 (update + gather); events (optional) after F1 and FX.
+cudaError_t launch_dp_fused(int32_t grad_dtype, const DevWork& wk, const DevScratch& sc, const Hyper& hy, float* w,
+                            float* m, const DpFused& f, int grid, cudaStream_t stream, cudaEvent_t ev1, cudaEvent_t ev2);
+
 // After the C3 allreduce: finish split layers, decide the global skip, advance a device iteration.
 cudaError_t launch_split_finish(const DevWork& wk, const DevScratch& sc, const Hyper& hy, cudaStream_t stream);
 cudaError_t launch_step(int32_t grad_dtype, const DevWork& wk, const DevScratch& sc, const Hyper& hy,

@@ -21,6 +21,9 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <nccl.h>
+#include <nccl_device.h>
+
 #include <cstdint>
 
 #include "internal.h"
@@ -142,6 +145,44 @@ extern "C" int lars_trace_arm(void* buf) {
 #define TRACE_END(k)
 #endif
 
+// ---------------------------------------------------------------- gradient sources for K1
+// Plain: the (already combined) gradient in local memory; element e lives at g[e - shift].
+template <int DT>
+struct LocalGrad {
+  const void* g;
+  int64_t shift;
+  __device__ __forceinline__ F8 load8(int64_t e) const { return Grad<DT>::load8_keep(g, e - shift); }
+  __device__ __forceinline__ float load1(int64_t e) const { return Grad<DT>::load1(g, e - shift); }
+};
+
+// Fused data-parallel reduce-scatter (dp fused path): element e of this rank's shard is the sum over the
+// P ranks' gradient buffers (symmetric NCCL window, read over NVLink), accumulated in fp32 in rank order;
+// the sum is also stored once into the local fp32 shard buffer the update kernel reads.
+constexpr int kMaxRanks = 8;
+template <int DT>
+struct PeerSumGrad {
+  const void* gp[kMaxRanks];  // gradient buffer of every rank (index = rank), same flat layout
+  int nranks;
+  float* gred;                // local fp32 reduced shard: element e at gred[e - begin]
+  int64_t begin;
+  __device__ __forceinline__ F8 load8(int64_t e) const {
+    F8 acc = Grad<DT>::load8(gp[0], e);
+    for (int p = 1; p < nranks; ++p) {
+      const F8 x = Grad<DT>::load8(gp[p], e);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc.v[i] += x.v[i];
+    }
+    st8(gred + (e - begin), acc);
+    return acc;
+  }
+  __device__ __forceinline__ float load1(int64_t e) const {
+    float acc = Grad<DT>::load1(gp[0], e);
+    for (int p = 1; p < nranks; ++p) acc += Grad<DT>::load1(gp[p], e);
+    gred[e - begin] = acc;
+    return acc;
+  }
+};
+
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
@@ -191,11 +232,10 @@ __device__ __forceinline__ bool finish_core(int32_t l, double sw, double sg, con
   return !(isfinite(wn) && isfinite(gn) && in_range);
 }
 
-template <int DT>
+template <class GL>
 __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, const DevScratch& sc, const Hyper& hy,
-                                           const float* __restrict__ w, const void* __restrict__ g,
-                                           int64_t g_shift, double* sm_cw, double* sm_cg, unsigned* sm_done,
-                                           unsigned* sm_nonfinite, bool carried) {
+                                           const float* __restrict__ w, const GL& gl, double* sm_cw,
+                                           double* sm_cg, unsigned* sm_done, unsigned* sm_nonfinite, bool carried) {
   constexpr int kWarps = kThreads / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // Phase A: the warps of the CTA stream the tile's chunks independently (no block barrier per layer);
@@ -204,7 +244,7 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
   for (int32_t c = c0 + warp; c < c1; c += kWarps) {
     const Seg ck = wk.chunks[c];
     const float* wp = w + ck.begin;
-    const int64_t gi = ck.begin - g_shift;
+    const int64_t gi = ck.begin;  // element index handed to the gradient source
     const int32_t ng = ck.len >> 3;
     if (carried) {  // sum(w^2) of this chunk was produced by the previous K2: stream g only
       double ag = 0.0, ag1 = 0.0;
@@ -212,16 +252,16 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
       for (; j + 96 < ng; j += 128) {  // 4 x 32 B in flight per lane
         F8 gv[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) gv[u] = Grad<DT>::load8_keep(g, gi + 8 * (j + 32 * u));
+        for (int u = 0; u < 4; ++u) gv[u] = gl.load8(gi + 8 * (j + 32 * u));
         acc8(ag, gv[0]);
         acc8(ag1, gv[1]);
         acc8(ag, gv[2]);
         acc8(ag1, gv[3]);
       }
-      for (; j < ng; j += 32) acc8(ag, Grad<DT>::load8_keep(g, gi + 8 * j));
+      for (; j < ng; j += 32) acc8(ag, gl.load8(gi + 8 * j));
       ag += ag1;
       for (int32_t i = (ng << 3) + lane; i < ck.len; i += 32) {
-        const double y = (double)Grad<DT>::load1(g, gi + i);
+        const double y = (double)gl.load1(gi + i);
         ag = fma(y, y, ag);
       }
 #pragma unroll
@@ -239,7 +279,7 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
 #pragma unroll
       for (int u = 0; u < kNormUnroll; ++u) {  // all loads first: 2*kNormUnroll x 32 B in flight per lane
         wv[u] = ld8_keep(wp + 8 * (j + u * 32));
-        gv[u] = Grad<DT>::load8_keep(g, gi + 8 * (j + u * 32));
+        gv[u] = gl.load8(gi + 8 * (j + u * 32));
       }
 #pragma unroll
       for (int u = 0; u < kNormUnroll; u += 2) {
@@ -253,14 +293,14 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
     }
     for (; j < ng; j += 32) {
       const F8 w0 = ld8_keep(wp + 8 * j);
-      const F8 g0 = Grad<DT>::load8_keep(g, gi + 8 * j);
+      const F8 g0 = gl.load8(gi + 8 * j);
       acc8(aw, w0);
       acc8(ag, g0);
     }
     aw += aw1;
     ag += ag1;
     for (int32_t i = (ng << 3) + lane; i < ck.len; i += 32) {  // ragged tensor tail (< 8 elements)
-      const double x = (double)wp[i], y = (double)Grad<DT>::load1(g, gi + i);
+      const double x = (double)wp[i], y = (double)gl.load1(gi + i);
       aw = fma(x, x, aw);
       ag = fma(y, y, ag);
     }
@@ -347,21 +387,19 @@ __device__ __forceinline__ int32_t take_ticket(unsigned long long* t, int32_t ni
   return (int32_t)(atomicAdd(t, 1ull) % (unsigned long long)(nitems + grid));
 }
 
-// K1. Persistent schedule: static (CTA b owns tiles b, b + grid, ...) or dynamic (kNormDynamic).
-template <int DT, bool CARRY>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_norms_kernel(DevWork wk, DevScratch sc, Hyper hy,
-                                                                          const float* __restrict__ w,
-                                                                          const void* __restrict__ g,
-                                                                          int64_t g_shift) {
+// K1 body, shared by the single-GPU / NCCL kernel and the fused data-parallel kernel (they differ only
+// in where the gradient comes from). Persistent schedule: static (CTA b owns tiles b, b + grid, ...) or
+// dynamic (kNormDynamic).
+template <bool CARRY, class GL>
+__device__ __forceinline__ void norms_body(const DevWork& wk, const DevScratch& sc, const Hyper& hy,
+                                           const float* __restrict__ w, const GL& gl) {
   __shared__ double sm_cw[kMaxTileChunks], sm_cg[kMaxTileChunks];
   __shared__ unsigned sm_done, sm_nonfinite;
-  pdl_trigger();
   if (threadIdx.x == 0) {
     sm_done = 0u;
     sm_nonfinite = 0u;
   }
-  pdl_wait();
-  TRACE_BEGIN
+  __syncthreads();
   // carry mode: the previous K2 left sum(w_new^2) per chunk; valid until the host invalidates it
   const bool carried = CARRY && *(volatile const int32_t*)sc.wnext_valid != 0;
   if (kNormDynamic) {  // tiles handed out by a ticket counter (faster CTAs take more tiles)
@@ -373,7 +411,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_norms_kernel(DevWor
       __syncthreads();  // s_tile read by all; shared chunk partials of the previous tile consumed
       int32_t next = 0;
       if (threadIdx.x == 0) next = take_ticket(sc.ticket + 0, wk.ntiles, gridDim.x);
-      norms_tile<DT>(tile, wk, sc, hy, w, g, g_shift, sm_cw, sm_cg, &sm_done, &sm_nonfinite, carried);
+      norms_tile(tile, wk, sc, hy, w, gl, sm_cw, sm_cg, &sm_done, &sm_nonfinite, carried);
       __syncthreads();
       if (threadIdx.x == 0) s_tile = next;
       __syncthreads();
@@ -382,11 +420,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_norms_kernel(DevWor
   } else {
     for (int32_t tile = blockIdx.x; tile < wk.ntiles; tile += gridDim.x) {
       __syncthreads();  // shared chunk partials of the previous tile fully consumed
-      norms_tile<DT>(tile, wk, sc, hy, w, g, g_shift, sm_cw, sm_cg, &sm_done, &sm_nonfinite, carried);
+      norms_tile(tile, wk, sc, hy, w, gl, sm_cw, sm_cg, &sm_done, &sm_nonfinite, carried);
     }
   }
   __syncthreads();
-  TRACE_END(0)
   // Count this CTA's finished layers once; the CTA that completes the count decides the step's skip.
   if (threadIdx.x == 0 && sm_done > 0u) {
     if (sm_nonfinite) atomicOr(sc.nonfinite, 1u);
@@ -396,7 +433,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_norms_kernel(DevWor
       __threadfence();
       const unsigned nf = atomicExch(sc.nonfinite, 0u);
       *(volatile unsigned*)sc.tensors_done = 0u;
-      if (sc.c3) {  // data parallel: the decision is global, taken after the C3 allreduce
+      if (sc.c3) {  // data parallel: the decision is global, taken after the C3 exchange
         *(volatile double*)sc.c3 = nf ? 1.0 : 0.0;
         return;
       }
@@ -409,6 +446,18 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_norms_kernel(DevWor
       *(volatile int32_t*)sc.skip = status;
     }
   }
+}
+
+template <int DT, bool CARRY>
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_norms_kernel(DevWork wk, DevScratch sc, Hyper hy,
+                                                                          const float* __restrict__ w,
+                                                                          const void* __restrict__ g,
+                                                                          int64_t g_shift) {
+  pdl_trigger();
+  pdl_wait();
+  TRACE_BEGIN
+  norms_body<CARRY>(wk, sc, hy, w, LocalGrad<DT>{g, g_shift});
+  TRACE_END(0)
 }
 
 // ---------------------------------------------------------------- K2: fused update
@@ -424,10 +473,34 @@ __device__ __forceinline__ void upd8(F8& w, F8& m, const F8& g, float s, float c
 
 __device__ __forceinline__ void accw8(double& a, const F8& x) { acc8(a, x); }
 
-template <int DT, bool CARRY>
+// Extra destinations of the updated weights: none (single GPU / NCCL all-gather), or every other rank's
+// weight buffer over NVLink (dp fused path: the all-gather happens as the update is written).
+struct NoPeers {
+  __device__ __forceinline__ void store8(int64_t, const F8&) const {}
+  __device__ __forceinline__ void store1(int64_t, float) const {}
+};
+struct PeerWeights {
+  float* pw[kMaxRanks - 1];  // the other ranks' weight buffers (symmetric window, same flat layout)
+  int n;
+  __device__ __forceinline__ void store8(int64_t e, const F8& x) const {
+    for (int p = 0; p < n; ++p) {
+      float* d = pw[p] + e;
+      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(d), "r"(__float_as_uint(x.v[0])),
+                   "r"(__float_as_uint(x.v[1])), "r"(__float_as_uint(x.v[2])), "r"(__float_as_uint(x.v[3])),
+                   "r"(__float_as_uint(x.v[4])), "r"(__float_as_uint(x.v[5])), "r"(__float_as_uint(x.v[6])),
+                   "r"(__float_as_uint(x.v[7]))
+                   : "memory");
+    }
+  }
+  __device__ __forceinline__ void store1(int64_t e, float x) const {
+    for (int p = 0; p < n; ++p) pw[p][e] = x;
+  }
+};
+
+template <int DT, bool CARRY, class WS = NoPeers>
 __device__ __forceinline__ void update_item(int32_t item, const DevWork& wk, const DevScratch& sc, const Hyper& hy,
                                             float* __restrict__ w, const void* __restrict__ g, int64_t g_shift,
-                                            float* __restrict__ m) {
+                                            float* __restrict__ m, const WS& ws = WS()) {
   constexpr int kWarps = kThreads / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float s = hy.grad_scale_f, mu = hy.mu;
@@ -451,6 +524,7 @@ __device__ __forceinline__ void update_item(int32_t item, const DevWork& wk, con
       const float v = fmaf(mu, mv, cf * u);
       wp[i] = wv - v;
       mp[i] = v;
+      ws.store1(ck.begin + i, wv - v);
       if (CARRY) aw = fma((double)(wv - v), (double)(wv - v), aw);
     }
     int32_t j = ng - 1 - lane;
@@ -465,6 +539,8 @@ __device__ __forceinline__ void update_item(int32_t item, const DevWork& wk, con
       st8(mp + 8 * j, m0);
       st8(wp + 8 * j1, w1);
       st8(mp + 8 * j1, m1);
+      ws.store8(ck.begin + 8 * j, w0);
+      ws.store8(ck.begin + 8 * j1, w1);
       if (CARRY) {
         accw8(aw, w0);
         accw8(aw1, w1);
@@ -476,6 +552,7 @@ __device__ __forceinline__ void update_item(int32_t item, const DevWork& wk, con
       upd8(w0, m0, g0, s, cf, b, mu);
       st8(wp + 8 * j, w0);
       st8(mp + 8 * j, m0);
+      ws.store8(ck.begin + 8 * j, w0);
       if (CARRY) accw8(aw, w0);
     }
     if (CARRY) {
@@ -519,7 +596,9 @@ __global__ void empty_step_kernel(int64_t* iter_dev, int64_t total_iters, int32_
 // Data-parallel finish, after C3 = allreduce(sum) of [non-finite count, split-layer partial sums]:
 // every rank sees the same global sums, so every rank takes the same skip decision (reading #13) and
 // each rank finishes the split layers it touches exactly like K1 finishes whole ones.
-__global__ void lars_split_finish_kernel(DevWork wk, DevScratch sc, Hyper hy) {
+// Consumes the global C3 sums in sc.c3 (one warp): every rank sees the same sums, so every rank takes the
+// same decision; zeroes sc.c3 for the next step's shares.
+__device__ __forceinline__ void split_finish_body(const DevWork& wk, const DevScratch& sc, const Hyper& hy) {
   const int lane = threadIdx.x;
   const int32_t n = 1 + 2 * wk.nsplit_total;
   bool bad = false;
@@ -543,6 +622,103 @@ __global__ void lars_split_finish_kernel(DevWork wk, DevScratch sc, Hyper hy) {
     }
     *sc.skip = status;
   }
+}
+
+__global__ void lars_split_finish_kernel(DevWork wk, DevScratch sc, Hyper hy) { split_finish_body(wk, sc, hy); }
+
+// ---------------------------------------------------------------- fused data-parallel path (NEXT-f1)
+// Gradient and weight buffers live in NCCL symmetric windows (ncclMemAlloc + ncclCommWindowRegister), so
+// every rank can load and store every other rank's buffers over NVLink with plain ld/st (LSA pointers).
+// The reduce-scatter is fused into K1 (each rank sums its shard over all ranks' gradients in fp32), the
+// C3 exchange is one warp storing its shares into every peer, and the all-gather is fused into K2 (each
+// updated weight is stored locally and into every peer). Per-CTA LSA barriers order the phases.
+//
+//   F1 lars_dp_reduce_norms_kernel : barrier(b) -> shard sum over ranks + norms (+ split shares)
+//   FX lars_dp_exchange_kernel     : C3 shares -> every peer, barrier, fixed-order sum, finish, skip
+//   F2 lars_dp_update_gather_kernel: update + store w to every peer -> barrier(b)
+template <int DT, bool CARRY>
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_dp_reduce_norms_kernel(DevWork wk, DevScratch sc,
+                                                                                    Hyper hy, const float* w,
+                                                                                    DpFused f) {
+  {  // CTA b of every rank is running => every rank's gradient for this step is complete
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), f.dc, ncclTeamTagLsa(), blockIdx.x);
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+  }
+  PeerSumGrad<DT> gl;
+  for (int p = 0; p < f.nranks; ++p) gl.gp[p] = ncclGetLsaPointer(f.gwin, 0, p);
+  gl.nranks = f.nranks;
+  gl.gred = f.gred;
+  gl.begin = f.begin;
+  norms_body<CARRY>(wk, sc, hy, w, gl);
+}
+
+__global__ void lars_dp_exchange_kernel(DevWork wk, DevScratch sc, Hyper hy, DpFused f, int barrier_index) {
+  const int lane = threadIdx.x;
+  const int32_t n = 1 + 2 * wk.nsplit_total;
+  for (int p = 0; p < f.nranks; ++p) {  // my shares into slot [rank] of every rank (myself included)
+    double* dst = (double*)ncclGetLsaPointer(f.xwin, (size_t)f.rank * n * sizeof(double), p);
+    for (int32_t i = lane; i < n; i += 32) dst[i] = sc.c3[i];
+  }
+  {
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), f.dc, ncclTeamTagLsa(), barrier_index);
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+  }
+  const double* x = (const double*)ncclGetLocalPointer(f.xwin, 0);
+  for (int32_t i = lane; i < n; i += 32) {
+    double t = 0.0;
+    for (int p = 0; p < f.nranks; ++p) t += x[(size_t)p * n + i];  // rank order: identical everywhere
+    sc.c3[i] = t;
+  }
+  __syncwarp();
+  split_finish_body(wk, sc, hy);
+}
+
+template <bool CARRY>
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_dp_update_gather_kernel(DevWork wk, DevScratch sc,
+                                                                                     Hyper hy, float* w, float* m,
+                                                                                     DpFused f) {
+  const bool skip = *(volatile const int32_t*)sc.skip != 0;
+  PeerWeights ws;
+  ws.n = 0;
+  for (int p = 0; p < f.nranks; ++p)
+    if (p != f.rank) ws.pw[ws.n++] = (float*)ncclGetLsaPointer(f.wwin, 0, p);
+  if (!skip)
+    for (int32_t tile = blockIdx.x; tile < wk.ntiles; tile += gridDim.x)
+      for (int32_t q = kUpdateSplit - 1; q >= 0; --q)
+        update_item<LARS_F32, CARRY, PeerWeights>((kUpdateSplit - 1 - q) * wk.ntiles + tile, wk, sc, hy, w, f.gred,
+                                                  f.begin, m, ws);
+  if (CARRY && !skip && blockIdx.x == 0 && threadIdx.x == 0) *(volatile int32_t*)sc.wnext_valid = 1;
+  {  // CTA b of every rank has stored its weights => after this grid, every rank's w is complete
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), f.dc, ncclTeamTagLsa(), blockIdx.x);
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+  }
+}
+
+cudaError_t launch_dp_fused(int32_t dt, const DevWork& wk, const DevScratch& sc, const Hyper& hy, float* w, float* m,
+                            const DpFused& f, int grid, cudaStream_t st, cudaEvent_t ev1, cudaEvent_t ev2) {
+  DevWork wg = wk;
+  wg.grid = grid;
+  if (hy.carry) {
+    switch (dt) {
+      case LARS_F32: lars_dp_reduce_norms_kernel<LARS_F32, true><<<grid, kThreads, 0, st>>>(wg, sc, hy, w, f); break;
+      case LARS_F16: lars_dp_reduce_norms_kernel<LARS_F16, true><<<grid, kThreads, 0, st>>>(wg, sc, hy, w, f); break;
+      default: lars_dp_reduce_norms_kernel<LARS_BF16, true><<<grid, kThreads, 0, st>>>(wg, sc, hy, w, f); break;
+    }
+  } else {
+    switch (dt) {
+      case LARS_F32: lars_dp_reduce_norms_kernel<LARS_F32, false><<<grid, kThreads, 0, st>>>(wg, sc, hy, w, f); break;
+      case LARS_F16: lars_dp_reduce_norms_kernel<LARS_F16, false><<<grid, kThreads, 0, st>>>(wg, sc, hy, w, f); break;
+      default: lars_dp_reduce_norms_kernel<LARS_BF16, false><<<grid, kThreads, 0, st>>>(wg, sc, hy, w, f); break;
+    }
+  }
+  if (ev1) cudaEventRecord(ev1, st);
+  lars_dp_exchange_kernel<<<1, 32, 0, st>>>(wg, sc, hy, f, grid);
+  if (ev2) cudaEventRecord(ev2, st);
+  if (hy.carry)
+    lars_dp_update_gather_kernel<true><<<grid, kThreads, 0, st>>>(wg, sc, hy, w, m, f);
+  else
+    lars_dp_update_gather_kernel<false><<<grid, kThreads, 0, st>>>(wg, sc, hy, w, m, f);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_split_finish(const DevWork& wk, const DevScratch& sc, const Hyper& hy, cudaStream_t st) {

@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <array>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -163,6 +164,19 @@ struct lars_ctx {
   cudaStream_t last_stream = nullptr;
   const DevBufs* last = nullptr;
   Profiler prof;
+  // fused data-parallel path (symmetric windows); set up by lars_comm_init when every rank is
+  // reachable over NVLink (NCCL LSA team == world) and LARS_DP_FUSED != 0
+  struct {
+    bool ok = false;
+    void *w = nullptr, *g = nullptr, *x = nullptr;
+    ncclWindow_t wwin = nullptr, gwin = nullptr, xwin = nullptr;
+    ncclDevComm dc{};
+    bool dc_ok = false;
+    float* gred32 = nullptr;
+    int grid = 0;
+  } fused;
+  int32_t last_red_dtype = LARS_F16;
+  const void* last_red = nullptr;
 };
 
 #define CUDA_OR(expr)                                      \
@@ -173,6 +187,40 @@ struct lars_ctx {
   do {                                                     \
     if ((expr) != ncclSuccess) return LARS_ERR_NCCL;       \
   } while (0)
+
+static size_t round4k(size_t b) { return (b + 4095) / 4096 * 4096; }
+
+// Symmetric buffers + windows + device communicator for the fused path. Collective over the comm.
+static lars_status_t setup_fused(lars_ctx* h) {
+  const char* env = getenv("LARS_DP_FUSED");
+  if (env && env[0] == '0') return LARS_OK;
+  if (h->plan.P > 8) return LARS_OK;  // kMaxRanks
+  ncclTeam_t lsa = ncclTeamLsa(h->comm);
+  if (lsa.nRanks != h->plan.P) return LARS_OK;  // not every rank on NVLink: keep the NCCL path
+  auto& f = h->fused;
+  const size_t wb = round4k((size_t)h->plan.padded * 4), gb = round4k((size_t)h->plan.padded * dtype_size(h->hp.grad_dtype));
+  const size_t xb = round4k((size_t)h->plan.P * (1 + 2 * (size_t)h->plan.nsplit) * sizeof(double));
+  NCCL_OR(ncclMemAlloc(&f.w, wb));
+  NCCL_OR(ncclMemAlloc(&f.g, gb));
+  NCCL_OR(ncclMemAlloc(&f.x, xb));
+  CUDA_OR(cudaMemset(f.w, 0, wb));
+  CUDA_OR(cudaMemset(f.g, 0, gb));
+  CUDA_OR(cudaMemset(f.x, 0, xb));
+  NCCL_OR(ncclCommWindowRegister(h->comm, f.w, wb, &f.wwin, NCCL_WIN_COLL_SYMMETRIC));
+  NCCL_OR(ncclCommWindowRegister(h->comm, f.g, gb, &f.gwin, NCCL_WIN_COLL_SYMMETRIC));
+  NCCL_OR(ncclCommWindowRegister(h->comm, f.x, xb, &f.xwin, NCCL_WIN_COLL_SYMMETRIC));
+  f.grid = h->sms * kCtasPerSm;  // one resident wave, identical on every rank (per-CTA barriers pair up)
+  ncclDevCommRequirements reqs;
+  std::memset(&reqs, 0, sizeof reqs);
+  reqs.lsaBarrierCount = f.grid + 1;
+  NCCL_OR(ncclDevCommCreate(h->comm, &reqs, &f.dc));
+  f.dc_ok = true;
+  if (cudaMalloc(&f.gred32, (size_t)h->plan.S * sizeof(float)) != cudaSuccess) return LARS_ERR_OOM;
+  CUDA_OR(cudaMemset(f.gred32, 0, (size_t)h->plan.S * sizeof(float)));
+  CUDA_OR(cudaDeviceSynchronize());
+  f.ok = true;
+  return LARS_OK;
+}
 
 static bool aligned256(const void* p) { return ((uintptr_t)p & 255u) == 0; }
 static ncclDataType_t nccl_type(int32_t dt) {
@@ -402,6 +450,8 @@ lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, cons
   if (cudaMalloc(&h->gred, (size_t)h->plan.S * dtype_size(h->hp.grad_dtype)) != cudaSuccess) return LARS_ERR_OOM;
   CUDA_OR(cudaMemset(h->gred, 0, (size_t)h->plan.S * dtype_size(h->hp.grad_dtype)));
   h->shard_ready = true;
+  st = setup_fused(h);
+  if (st != LARS_OK) return st;
   return LARS_OK;
 }
 
@@ -414,6 +464,22 @@ static lars_status_t dp_impl(lars_handle_t h, float* w, const void* g, float* m,
   lars_status_t cg = carry_guard(h, h->shard, w, s);
   if (cg != LARS_OK) return cg;
   auto* pe = h->prof.begin(2);
+  if (h->fused.ok && (void*)w == h->fused.w && g == h->fused.g) {  // fused NVLink path (F1, FX, F2)
+    DpFused f{h->fused.dc, h->fused.gwin, h->fused.wwin, h->fused.xwin, h->rank, h->plan.P, begin, h->fused.gred32};
+    prof_rec(pe, 0, s);
+    prof_rec(pe, 1, s);
+    CUDA_OR(launch_dp_fused(dt, h->shard.dw, h->shard.sc, hy, w, m, f, h->fused.grid, s, pe ? (*pe)[2] : nullptr,
+                            pe ? (*pe)[3] : nullptr));
+    if (pe) {
+      cudaEventRecord((*pe)[4], s);
+      cudaEventRecord((*pe)[5], s);
+    }
+    h->last_stream = s;
+    h->last = &h->shard;
+    h->last_red = h->fused.gred32;
+    h->last_red_dtype = LARS_F32;
+    return LARS_OK;
+  }
   prof_rec(pe, 0, s);
   NCCL_OR(ncclReduceScatter(g, h->gred, (size_t)S, nccl_type(dt), ncclSum, h->comm, s));          // C1
   prof_rec(pe, 1, s);
@@ -429,6 +495,8 @@ static lars_status_t dp_impl(lars_handle_t h, float* w, const void* g, float* m,
   prof_rec(pe, 5, s);
   h->last_stream = s;
   h->last = &h->shard;
+  h->last_red = h->gred;
+  h->last_red_dtype = dt;
   return LARS_OK;
 }
 
@@ -476,9 +544,22 @@ lars_status_t dp_allreduce_lars_step_host_grad(lars_handle_t h, float* w, const 
   if (!h->comm || !h->shard_ready) return LARS_ERR_NO_COMM;
   DeviceGuard dg(h->device);
   cudaStream_t s = (cudaStream_t)stream;
-  lars_status_t st = stage_host_grad(h, g_host, s);
-  if (st != LARS_OK) return st;
-  st = dp_allreduce_lars_step(h, w, h->gstage, m, iter, stream);
+  lars_status_t st;
+  const void* gdev;
+  if (h->fused.ok && (void*)w == h->fused.w) {  // fused path: the gradient lands in the symmetric buffer
+    const size_t gbytes = (size_t)h->plan.padded * dtype_size(h->hp.grad_dtype);
+    if (!h->pinned && cudaMallocHost(&h->pinned, 256 + 2 * (size_t)h->plan.L * sizeof(double)) != cudaSuccess) {
+      h->pinned = nullptr;
+      return LARS_ERR_OOM;
+    }
+    CUDA_OR(cudaMemcpyAsync(h->fused.g, g_host, gbytes, cudaMemcpyHostToDevice, s));
+    gdev = h->fused.g;
+  } else {
+    st = stage_host_grad(h, g_host, s);
+    if (st != LARS_OK) return st;
+    gdev = h->gstage;
+  }
+  st = dp_allreduce_lars_step(h, w, gdev, m, iter, stream);
   if (st != LARS_OK) return st;
   return readback_status(h, h->shard, s);
 }
@@ -524,10 +605,19 @@ lars_status_t lars_profile_read(lars_handle_t h, double* ms, int64_t* steps) {
   return LARS_OK;
 }
 
-lars_status_t lars_reduced_grad(lars_handle_t h, const void** dev_ptr, int64_t* begin, int64_t* end) {
+lars_status_t lars_dp_buffers(lars_handle_t h, float** w, void** g) {
+  if (!h) return LARS_ERR_INVALID_ARG;
+  if (!h->fused.ok) return LARS_ERR_NO_COMM;
+  if (w) *w = (float*)h->fused.w;
+  if (g) *g = h->fused.g;
+  return LARS_OK;
+}
+
+lars_status_t lars_reduced_grad(lars_handle_t h, const void** dev_ptr, int32_t* dtype, int64_t* begin, int64_t* end) {
   if (!h || !dev_ptr) return LARS_ERR_INVALID_ARG;
   if (!h->gred) return LARS_ERR_NO_COMM;
-  *dev_ptr = h->gred;
+  *dev_ptr = h->last_red ? h->last_red : h->gred;
+  if (dtype) *dtype = h->last_red ? h->last_red_dtype : h->hp.grad_dtype;
   if (begin) *begin = (int64_t)h->rank * h->plan.S;
   if (end) *end = (int64_t)(h->rank + 1) * h->plan.S;
   return LARS_OK;
@@ -579,7 +669,18 @@ lars_status_t lars_destroy(lars_handle_t h) {
   if (!h) return LARS_ERR_INVALID_ARG;
   if (h->device >= 0) {
     DeviceGuard dg(h->device);
-    if (h->comm) ncclCommDestroy(h->comm);
+    if (h->comm) {
+      auto& f = h->fused;
+      if (f.dc_ok) ncclDevCommDestroy(h->comm, &f.dc);
+      if (f.wwin) ncclCommWindowDeregister(h->comm, f.wwin);
+      if (f.gwin) ncclCommWindowDeregister(h->comm, f.gwin);
+      if (f.xwin) ncclCommWindowDeregister(h->comm, f.xwin);
+      if (f.w) ncclMemFree(f.w);
+      if (f.g) ncclMemFree(f.g);
+      if (f.x) ncclMemFree(f.x);
+      cudaFree(f.gred32);
+      ncclCommDestroy(h->comm);
+    }
     cudaFree(h->lr_d);
     cudaFree(h->full.mem);
     cudaFree(h->shard.mem);

@@ -79,7 +79,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "dp_allreduce_lars_step_host_grad": (c_int32, [h, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
         "lars_profile_enable": (c_int32, [h, c_int32]),
         "lars_profile_read": (c_int32, [h, POINTER(c_double), POINTER(c_int64)]),
-        "lars_reduced_grad": (c_int32, [h, POINTER(c_void_p), POINTER(c_int64), POINTER(c_int64)]),
+        "lars_reduced_grad": (c_int32, [h, POINTER(c_void_p), POINTER(c_int32), POINTER(c_int64), POINTER(c_int64)]),
+        "lars_dp_buffers": (c_int32, [h, POINTER(c_void_p), POINTER(c_void_p)]),
         "lars_last_norms": (c_int32, [h, POINTER(c_double), POINTER(c_double), POINTER(c_double),
                                       POINTER(c_double)]),
         "lars_last_step_skipped": (c_int32, [h, POINTER(c_int32)]),
@@ -269,11 +270,24 @@ class Lars:
         """torch view of the library's reduced-gradient shard (last dp step) and its [begin, end)."""
         import torch
 
-        p, b, e = c_void_p(), c_int64(), c_int64()
-        _check(self._lib.lars_reduced_grad(self._h, byref(p), byref(b), byref(e)), "lars_reduced_grad")
-        typestr = {"f32": "<f4", "f16": "<f2", "bf16": "<i2"}[self.grad_dtype]
+        p, dt, b, e = c_void_p(), c_int32(), c_int64(), c_int64()
+        _check(self._lib.lars_reduced_grad(self._h, byref(p), byref(dt), byref(b), byref(e)), "lars_reduced_grad")
+        typestr = {0: "<f4", 1: "<f2", 2: "<i2"}[int(dt.value)]
         t = torch.as_tensor(_DevView(p.value, int(e.value - b.value), typestr), device=f"cuda:{self.device}")
         return t, int(b.value), int(e.value)
+
+    def dp_buffers(self):
+        """torch views of the library-owned symmetric weight and gradient buffers (fused NVLink path);
+        raises LarsError(LARS_ERR_NO_COMM) when the fused path is unavailable."""
+        import torch
+
+        wp, gp = c_void_p(), c_void_p()
+        _check(self._lib.lars_dp_buffers(self._h, byref(wp), byref(gp)), "lars_dp_buffers")
+        dev = f"cuda:{self.device}"
+        w = torch.as_tensor(_DevView(wp.value, self.padded_numel, "<f4"), device=dev)
+        g = torch.as_tensor(_DevView(gp.value, self.padded_numel, {"f32": "<f4", "f16": "<f2", "bf16": "<i2"}[
+            self.grad_dtype]), device=dev)
+        return w, g
 
     # ---- readbacks (synchronize) ----
     def last_norms(self):

@@ -47,7 +47,7 @@ def main():
         dist.all_reduce(hi, op=dist.ReduceOp.MAX)
         return bool(torch.equal(lo, hi))
 
-    def run_case(name, lay, dtype, t, kind="random", inject_nan=False, **hpkw):
+    def run_case(name, lay, dtype, t, kind="random", inject_nan=False, fused=False, **hpkw):
         kw = hp_kwargs(grad_dtype=dtype, grad_scale=1.0 / (G.GRAD_PRESCALE * P), **hpkw)
         h = PK.Lars([(x.numel, x.kind) for x in lay], device=local, nranks=P, **kw)
         h.comm_init_torch()
@@ -67,19 +67,27 @@ def main():
         pack = lambda a: torch.from_numpy(G.pack(a, h.offsets, h.padded_numel).view(
             np.int16 if a[0].dtype == np.uint16 else a[0].dtype)).to(dev)
         w, g, m = pack(w_l), pack(g_all[rank]), pack(m_l)
+        if fused:  # library-owned symmetric buffers: the fused NVLink path (F1, FX, F2)
+            w_sym, g_sym = h.dp_buffers()
+            w_sym.copy_(w)
+            g_sym.copy_(g)
+            w, g = w_sym, g_sym
+            torch.cuda.synchronize()
         g_before = g.clone()
         h.dp_allreduce_lars_step(w, g, m, t)
         torch.cuda.synchronize()
         res = {"name": name, "dtype": dtype, "t": t}
         same = all_same(w)  # collectives first: every rank calls them before any rank-local assertion
         red_t, b, e = h.reduced_grad()
+        red_dtype = {torch.float32: "f32", torch.float16: "f16", torch.int16: "bf16"}[red_t.dtype]
         if red_t.dtype == torch.int16:  # bf16 bit patterns travel as fp16 words (bit-preserving)
             red_t = red_t.view(torch.float16)
         parts = [torch.empty_like(red_t) for _ in range(P)]
         dist.all_gather(parts, red_t.clone())
         full_red = from_dev(torch.cat(parts))  # the exact buffer every K1 read, all shards
-        if dtype == "bf16":
+        if red_dtype == "bf16":
             full_red = full_red.view(np.uint16)
+        res["reduced_dtype"] = red_dtype
         assert torch.equal(g.view(torch.int16) if g.element_size() == 2 else g.view(torch.int32),
                            g_before.view(torch.int16) if g.element_size() == 2 else g_before.view(torch.int32)), \
             "dp step modified the caller's gradient"
@@ -111,10 +119,11 @@ def main():
             lo, hi = pieces[l]
             got = O.to_double(full_red[h.offsets[l] + lo: h.offsets[l] + hi])
             exact = O.combine([g_all[r][l][lo:hi] for r in range(P)], 1.0)
-            if kind == "integer" and dtype != "bf16":
+            if kind == "integer" and red_dtype != "bf16":
                 assert np.array_equal(got, exact), f"{name}: integer sum not exact (tensor {l})"
             else:
-                bound = (P - 1) * (2.0 ** -11 if dtype == "f16" else 2.0 ** -8 if dtype == "bf16" else 2.0 ** -24) \
+                u = {"f16": 2.0 ** -11, "bf16": 2.0 ** -8, "f32": 2.0 ** -24}[red_dtype]
+                bound = (P - 1) * u \
                     * sum(np.abs(O.to_double(g_all[r][l][lo:hi])) for r in range(P))
                 err = np.abs(got - exact)
                 assert (err <= bound).all(), f"{name}: reduction error above the (P-1)u sum|g| bound at tensor {l}"
@@ -149,6 +158,13 @@ def main():
              ("r50-lpt-f16", lay_r50, "f16", 80, dict(shard_policy="lpt")),
              ("zipf-f16", LY.skew1b("zipf", n_tensors=200, total=4_000_000), "f16", 500, {}),
              ("nan-on-rank1", LY.tiny(), "f16", 100, dict(inject_nan=True)),
+             ("fused-tiny-int", LY.tiny(), "f16", 80, dict(kind="integer", fused=True)),
+             ("fused-r50-f16", lay_r50, "f16", 719, dict(fused=True)),
+             ("fused-r50-f16-carry", lay_r50, "f16", 720, dict(fused=True, flags=1)),
+             ("fused-random-bf16", LY.random_layout(np.random.default_rng(8), 29), "bf16", 700, dict(fused=True)),
+             ("fused-zipf-f32", LY.skew1b("zipf", n_tensors=200, total=4_000_000), "f32", 500, dict(fused=True)),
+             ("fused-nan-in-split-layer", LY.skew1b("zipf", n_tensors=50, total=1_000_000), "f16", 100,
+              dict(inject_nan="split", fused=True)),
              ("nan-in-split-layer", LY.skew1b("zipf", n_tensors=50, total=1_000_000), "f16", 100,
               dict(inject_nan="split"))]
     for name, lay, dtype, t, kw in cases:
