@@ -23,6 +23,8 @@ constexpr int kThreads = 256;           // threads per CTA of K1 / K2
 #define LARS_NORM_UNROLL 2
 #endif
 constexpr int kCtasPerSm = LARS_NORM_CTAS_PER_SM;      // K1 resident CTAs per SM (one static tile each)
+// fused F1 CTAs per SM: 2 ranks fit 64 registers (4 CTAs/SM); 3-8 ranks' loads per vector need 128 (2/SM)
+constexpr int dp_norm_ctas_per_sm(int nranks) { return nranks <= 2 ? 4 : 2; }
 #ifndef LARS_NORM_TILES_PER_CTA
 #define LARS_NORM_TILES_PER_CTA 1
 #endif
@@ -156,9 +158,12 @@ struct DpFused {
   int64_t begin;                  // first element of this rank's shard
   float* gred;                    // fp32 reduced shard (S elements)
 };
-// F1 (reduce + norms), FX (exchange + finish), F2 (update + gather); events (optional) after F1 and FX.
+// F1 (reduce + norms, grid_norm CTAs), FX (exchange + finish), F2 (update + gather, grid_update CTAs);
+// both grids identical on every rank (the per-CTA LSA barriers pair CTA b with CTA b of every rank).
+// Events (optional) are recorded after F1 and FX.
 cudaError_t launch_dp_fused(int32_t grad_dtype, const DevWork& wk, const DevScratch& sc, const Hyper& hy, float* w,
-                            float* m, const DpFused& f, int grid, cudaStream_t stream, cudaEvent_t ev1, cudaEvent_t ev2);
+                            float* m, const DpFused& f, int grid_norm, int grid_update, cudaStream_t stream,
+                            cudaEvent_t ev1, cudaEvent_t ev2);
 
 // After the C3 allreduce: finish split layers, decide the global skip, advance a device iteration.
 cudaError_t launch_split_finish(const DevWork& wk, const DevScratch& sc, const Hyper& hy, cudaStream_t stream);

@@ -70,6 +70,13 @@ __device__ __forceinline__ void st8(float* p, const F8& o) {
                "r"(__float_as_uint(o.v[6])), "r"(__float_as_uint(o.v[7]))
                : "memory");
 }
+// Store with no compiler memory clobber: lets later (non-aliasing) loads be hoisted above it.
+__device__ __forceinline__ void st8_noclobber(float* p, const F8& o) {
+  asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+               ::"l"(p), "r"(__float_as_uint(o.v[0])), "r"(__float_as_uint(o.v[1])), "r"(__float_as_uint(o.v[2])),
+               "r"(__float_as_uint(o.v[3])), "r"(__float_as_uint(o.v[4])), "r"(__float_as_uint(o.v[5])),
+               "r"(__float_as_uint(o.v[6])), "r"(__float_as_uint(o.v[7])));
+}
 __device__ __forceinline__ uint4 ld16_nc(const void* p) {
   uint4 r;
   asm("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
@@ -79,10 +86,16 @@ __device__ __forceinline__ uint4 ld16_nc(const void* p) {
 
 // Gradient access by wire dtype. Widening fp16/bf16 -> fp32 is exact.
 template <int DT> struct Grad;
+// Raw (undecoded) 8-element vectors: lets a caller issue many loads before decoding any of them.
+template <int DT> struct GradRaw { using T = uint4; };
+template <> struct GradRaw<LARS_F32> { using T = F8; };
+
 template <> struct Grad<LARS_F32> {
   __device__ __forceinline__ static F8 load8_keep(const void* g, int64_t i) { return ld8_keep((const float*)g + i); }
   __device__ __forceinline__ static F8 load8(const void* g, int64_t i) { return ld8_nc((const float*)g + i); }
   __device__ __forceinline__ static float load1(const void* g, int64_t i) { return __ldg((const float*)g + i); }
+  __device__ __forceinline__ static F8 raw8(const void* g, int64_t i) { return ld8_nc((const float*)g + i); }
+  __device__ __forceinline__ static F8 widen(const F8& r) { return r; }
 };
 __device__ __forceinline__ F8 widen_h8(uint4 r) {
   F8 o;
@@ -109,6 +122,8 @@ template <> struct Grad<LARS_F16> {
   __device__ __forceinline__ static F8 load8_keep(const void* g, int64_t i) { return widen_h8(ld16_nc((const __half*)g + i)); }
   __device__ __forceinline__ static F8 load8(const void* g, int64_t i) { return widen_h8(ld16_nc((const __half*)g + i)); }
   __device__ __forceinline__ static float load1(const void* g, int64_t i) { return __half2float(((const __half*)g)[i]); }
+  __device__ __forceinline__ static uint4 raw8(const void* g, int64_t i) { return ld16_nc((const __half*)g + i); }
+  __device__ __forceinline__ static F8 widen(const uint4& r) { return widen_h8(r); }
 };
 template <> struct Grad<LARS_BF16> {
   __device__ __forceinline__ static F8 load8_keep(const void* g, int64_t i) { return widen_b8(ld16_nc((const uint16_t*)g + i)); }
@@ -116,6 +131,8 @@ template <> struct Grad<LARS_BF16> {
   __device__ __forceinline__ static float load1(const void* g, int64_t i) {
     return __uint_as_float((uint32_t)((const uint16_t*)g)[i] << 16);
   }
+  __device__ __forceinline__ static uint4 raw8(const void* g, int64_t i) { return ld16_nc((const uint16_t*)g + i); }
+  __device__ __forceinline__ static F8 widen(const uint4& r) { return widen_b8(r); }
 };
 
 #ifdef LARS_TRACE
@@ -149,6 +166,8 @@ extern "C" int lars_trace_arm(void* buf) {
 // Plain: the (already combined) gradient in local memory; element e lives at g[e - shift].
 template <int DT>
 struct LocalGrad {
+  static constexpr int kUnroll = kNormUnroll;  // (w, g) groups per lane per iteration
+  static constexpr int kUnrollG = 4;           // g-only groups per lane per iteration (carried norms)
   const void* g;
   int64_t shift;
   __device__ __forceinline__ F8 load8(int64_t e) const { return Grad<DT>::load8_keep(g, e - shift); }
@@ -159,25 +178,39 @@ struct LocalGrad {
 // P ranks' gradient buffers (symmetric NCCL window, read over NVLink), accumulated in fp32 in rank order;
 // the sum is also stored once into the local fp32 shard buffer the update kernel reads.
 constexpr int kMaxRanks = 8;
-template <int DT>
+template <int DT, int NP>  // NP: compile-time upper bound of the rank count (2, 4 or 8)
 struct PeerSumGrad {
-  const void* gp[kMaxRanks];  // gradient buffer of every rank (index = rank), same flat layout
+  const void* gp[NP];         // gradient buffer of every rank (index = rank < nranks), same flat layout
   int nranks;
   float* gred;                // local fp32 reduced shard: element e at gred[e - begin]
   int64_t begin;
+  static constexpr int kUnroll = 1;                 // (w, g) groups per lane per iteration (register budget)
+  static constexpr int kUnrollG = NP <= 2 ? 2 : 1;  // g-only groups per lane per iteration (carried norms)
+  static constexpr int kBatch = NP < 4 ? NP : 4;   // peer loads issued back to back before decoding
   __device__ __forceinline__ F8 load8(int64_t e) const {
-    F8 acc = Grad<DT>::load8(gp[0], e);
-    for (int p = 1; p < nranks; ++p) {
-      const F8 x = Grad<DT>::load8(gp[p], e);
+    F8 acc;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc.v[i] += x.v[i];
+    for (int i = 0; i < 8; ++i) acc.v[i] = 0.f;
+#pragma unroll
+    for (int p0 = 0; p0 < NP; p0 += kBatch) {  // rank order 0..nranks-1, in batches of kBatch loads
+      typename GradRaw<DT>::T r[kBatch];
+#pragma unroll
+      for (int q = 0; q < kBatch; ++q)
+        if (p0 + q < nranks) r[q] = Grad<DT>::raw8(gp[p0 + q], e);
+#pragma unroll
+      for (int q = 0; q < kBatch; ++q)
+        if (p0 + q < nranks) {
+          const F8 x = Grad<DT>::widen(r[q]);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc.v[i] += x.v[i];
+        }
     }
-    st8(gred + (e - begin), acc);
+    st8_noclobber(gred + (e - begin), acc);
     return acc;
   }
   __device__ __forceinline__ float load1(int64_t e) const {
-    float acc = Grad<DT>::load1(gp[0], e);
-    for (int p = 1; p < nranks; ++p) acc += Grad<DT>::load1(gp[p], e);
+    float acc = 0.f;
+    for (int p = 0; p < nranks; ++p) acc += Grad<DT>::load1(gp[p], e);
     gred[e - begin] = acc;
     return acc;
   }
@@ -249,14 +282,16 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
     if (carried) {  // sum(w^2) of this chunk was produced by the previous K2: stream g only
       double ag = 0.0, ag1 = 0.0;
       int32_t j = lane;
-      for (; j + 96 < ng; j += 128) {  // 4 x 32 B in flight per lane
-        F8 gv[4];
+      constexpr int U = GL::kUnrollG;  // local source: 4 x 32 B in flight per lane
+      for (; j + (U - 1) * 32 < ng; j += U * 32) {
+        F8 gv[U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) gv[u] = gl.load8(gi + 8 * (j + 32 * u));
-        acc8(ag, gv[0]);
-        acc8(ag1, gv[1]);
-        acc8(ag, gv[2]);
-        acc8(ag1, gv[3]);
+        for (int u = 0; u < U; ++u) gv[u] = gl.load8(gi + 8 * (j + 32 * u));
+#pragma unroll
+        for (int u = 0; u < U; u += 2) {
+          acc8(ag, gv[u]);
+          if (u + 1 < U) acc8(ag1, gv[u + 1]);
+        }
       }
       for (; j < ng; j += 32) acc8(ag, gl.load8(gi + 8 * j));
       ag += ag1;
@@ -274,18 +309,19 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
     }
     double aw = 0.0, ag = 0.0, aw1 = 0.0, ag1 = 0.0;
     int32_t j = lane;
-    for (; j + (kNormUnroll - 1) * 32 < ng; j += kNormUnroll * 32) {
-      F8 wv[kNormUnroll], gv[kNormUnroll];
+    constexpr int U = GL::kUnroll;
+    for (; j + (U - 1) * 32 < ng; j += U * 32) {
+      F8 wv[U], gv[U];
 #pragma unroll
-      for (int u = 0; u < kNormUnroll; ++u) {  // all loads first: 2*kNormUnroll x 32 B in flight per lane
+      for (int u = 0; u < U; ++u) {  // all loads first: 2*U x 32 B in flight per lane
         wv[u] = ld8_keep(wp + 8 * (j + u * 32));
         gv[u] = gl.load8(gi + 8 * (j + u * 32));
       }
 #pragma unroll
-      for (int u = 0; u < kNormUnroll; u += 2) {
+      for (int u = 0; u < U; u += 2) {
         acc8(aw, wv[u]);
         acc8(ag, gv[u]);
-        if (u + 1 < kNormUnroll) {
+        if (u + 1 < U) {
           acc8(aw1, wv[u + 1]);
           acc8(ag1, gv[u + 1]);
         }
@@ -636,16 +672,17 @@ __global__ void lars_split_finish_kernel(DevWork wk, DevScratch sc, Hyper hy) { 
 //   F1 lars_dp_reduce_norms_kernel : barrier(b) -> shard sum over ranks + norms (+ split shares)
 //   FX lars_dp_exchange_kernel     : C3 shares -> every peer, barrier, fixed-order sum, finish, skip
 //   F2 lars_dp_update_gather_kernel: update + store w to every peer -> barrier(b)
-template <int DT, bool CARRY>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_dp_reduce_norms_kernel(DevWork wk, DevScratch sc,
+template <int DT, bool CARRY, int NP>
+__global__ void __launch_bounds__(kThreads, dp_norm_ctas_per_sm(NP)) lars_dp_reduce_norms_kernel(DevWork wk, DevScratch sc,
                                                                                     Hyper hy, const float* w,
                                                                                     DpFused f) {
   {  // CTA b of every rank is running => every rank's gradient for this step is complete
     ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), f.dc, ncclTeamTagLsa(), blockIdx.x);
     bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
   }
-  PeerSumGrad<DT> gl;
-  for (int p = 0; p < f.nranks; ++p) gl.gp[p] = ncclGetLsaPointer(f.gwin, 0, p);
+  PeerSumGrad<DT, NP> gl;
+#pragma unroll
+  for (int p = 0; p < NP; ++p) gl.gp[p] = p < f.nranks ? ncclGetLsaPointer(f.gwin, 0, p) : nullptr;
   gl.nranks = f.nranks;
   gl.gred = f.gred;
   gl.begin = f.begin;
@@ -682,11 +719,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_dp_update_gather_ke
   ws.n = 0;
   for (int p = 0; p < f.nranks; ++p)
     if (p != f.rank) ws.pw[ws.n++] = (float*)ncclGetLsaPointer(f.wwin, 0, p);
-  if (!skip)
-    for (int32_t tile = blockIdx.x; tile < wk.ntiles; tile += gridDim.x)
-      for (int32_t q = kUpdateSplit - 1; q >= 0; --q)
-        update_item<LARS_F32, CARRY, PeerWeights>((kUpdateSplit - 1 - q) * wk.ntiles + tile, wk, sc, hy, w, f.gred,
-                                                  f.begin, m, ws);
+  if (!skip)  // items ordered last-part-of-every-tile first (see update_item), striped over this grid
+    for (int32_t item = blockIdx.x; item < wk.ntiles * kUpdateSplit; item += gridDim.x)
+      update_item<LARS_F32, CARRY, PeerWeights>(item, wk, sc, hy, w, f.gred, f.begin, m, ws);
   if (CARRY && !skip && blockIdx.x == 0 && threadIdx.x == 0) *(volatile int32_t*)sc.wnext_valid = 1;
   {  // CTA b of every rank has stored its weights => after this grid, every rank's w is complete
     ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), f.dc, ncclTeamTagLsa(), blockIdx.x);
@@ -694,30 +729,43 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_dp_update_gather_ke
   }
 }
 
-cudaError_t launch_dp_fused(int32_t dt, const DevWork& wk, const DevScratch& sc, const Hyper& hy, float* w, float* m,
-                            const DpFused& f, int grid, cudaStream_t st, cudaEvent_t ev1, cudaEvent_t ev2) {
-  DevWork wg = wk;
-  wg.grid = grid;
-  if (hy.carry) {
-    switch (dt) {
-      case LARS_F32: lars_dp_reduce_norms_kernel<LARS_F32, true><<<grid, kThreads, 0, st>>>(wg, sc, hy, w, f); break;
-      case LARS_F16: lars_dp_reduce_norms_kernel<LARS_F16, true><<<grid, kThreads, 0, st>>>(wg, sc, hy, w, f); break;
-      default: lars_dp_reduce_norms_kernel<LARS_BF16, true><<<grid, kThreads, 0, st>>>(wg, sc, hy, w, f); break;
-    }
+template <int DT, bool CARRY>
+static void launch_reduce_norms_np(int np, int grid, cudaStream_t st, const DevWork& wk, const DevScratch& sc,
+                                   const Hyper& hy, const float* w, const DpFused& f) {
+  if (np <= 2)
+    lars_dp_reduce_norms_kernel<DT, CARRY, 2><<<grid, kThreads, 0, st>>>(wk, sc, hy, w, f);
+  else if (np <= 4)
+    lars_dp_reduce_norms_kernel<DT, CARRY, 4><<<grid, kThreads, 0, st>>>(wk, sc, hy, w, f);
+  else
+    lars_dp_reduce_norms_kernel<DT, CARRY, 8><<<grid, kThreads, 0, st>>>(wk, sc, hy, w, f);
+}
+
+static void launch_reduce_norms(int32_t dt, bool carry, int np, int grid, cudaStream_t st, const DevWork& wk,
+                                const DevScratch& sc, const Hyper& hy, const float* w, const DpFused& f) {
+  if (carry) {
+    if (dt == LARS_F32) launch_reduce_norms_np<LARS_F32, true>(np, grid, st, wk, sc, hy, w, f);
+    else if (dt == LARS_F16) launch_reduce_norms_np<LARS_F16, true>(np, grid, st, wk, sc, hy, w, f);
+    else launch_reduce_norms_np<LARS_BF16, true>(np, grid, st, wk, sc, hy, w, f);
   } else {
-    switch (dt) {
-      case LARS_F32: lars_dp_reduce_norms_kernel<LARS_F32, false><<<grid, kThreads, 0, st>>>(wg, sc, hy, w, f); break;
-      case LARS_F16: lars_dp_reduce_norms_kernel<LARS_F16, false><<<grid, kThreads, 0, st>>>(wg, sc, hy, w, f); break;
-      default: lars_dp_reduce_norms_kernel<LARS_BF16, false><<<grid, kThreads, 0, st>>>(wg, sc, hy, w, f); break;
-    }
+    if (dt == LARS_F32) launch_reduce_norms_np<LARS_F32, false>(np, grid, st, wk, sc, hy, w, f);
+    else if (dt == LARS_F16) launch_reduce_norms_np<LARS_F16, false>(np, grid, st, wk, sc, hy, w, f);
+    else launch_reduce_norms_np<LARS_BF16, false>(np, grid, st, wk, sc, hy, w, f);
   }
+}
+
+cudaError_t launch_dp_fused(int32_t dt, const DevWork& wk, const DevScratch& sc, const Hyper& hy, float* w, float* m,
+                            const DpFused& f, int grid_norm, int grid_update, cudaStream_t st, cudaEvent_t ev1,
+                            cudaEvent_t ev2) {
+  DevWork wg = wk;
+  wg.grid = grid_norm;
+  launch_reduce_norms(dt, hy.carry, f.nranks, grid_norm, st, wg, sc, hy, w, f);
   if (ev1) cudaEventRecord(ev1, st);
-  lars_dp_exchange_kernel<<<1, 32, 0, st>>>(wg, sc, hy, f, grid);
+  lars_dp_exchange_kernel<<<1, 32, 0, st>>>(wg, sc, hy, f, grid_update);
   if (ev2) cudaEventRecord(ev2, st);
   if (hy.carry)
-    lars_dp_update_gather_kernel<true><<<grid, kThreads, 0, st>>>(wg, sc, hy, w, m, f);
+    lars_dp_update_gather_kernel<true><<<grid_update, kThreads, 0, st>>>(wg, sc, hy, w, m, f);
   else
-    lars_dp_update_gather_kernel<false><<<grid, kThreads, 0, st>>>(wg, sc, hy, w, m, f);
+    lars_dp_update_gather_kernel<false><<<grid_update, kThreads, 0, st>>>(wg, sc, hy, w, m, f);
   return cudaGetLastError();
 }
 

@@ -173,7 +173,7 @@ struct lars_ctx {
     ncclDevComm dc{};
     bool dc_ok = false;
     float* gred32 = nullptr;
-    int grid = 0;
+    int grid_norm = 0, grid_update = 0;
   } fused;
   int32_t last_red_dtype = LARS_F16;
   const void* last_red = nullptr;
@@ -191,12 +191,14 @@ struct lars_ctx {
 static size_t round4k(size_t b) { return (b + 4095) / 4096 * 4096; }
 
 // Symmetric buffers + windows + device communicator for the fused path. Collective over the comm.
-static lars_status_t setup_fused(lars_ctx* h) {
+static bool fused_eligible(lars_ctx* h) {
   const char* env = getenv("LARS_DP_FUSED");
-  if (env && env[0] == '0') return LARS_OK;
-  if (h->plan.P > 8) return LARS_OK;  // kMaxRanks
-  ncclTeam_t lsa = ncclTeamLsa(h->comm);
-  if (lsa.nRanks != h->plan.P) return LARS_OK;  // not every rank on NVLink: keep the NCCL path
+  if (env && env[0] == '0') return false;
+  if (h->plan.P > 8) return false;  // kMaxRanks
+  return ncclTeamLsa(h->comm).nRanks == h->plan.P;  // every rank on one NVLink domain
+}
+
+static lars_status_t setup_fused(lars_ctx* h) {
   auto& f = h->fused;
   const size_t wb = round4k((size_t)h->plan.padded * 4), gb = round4k((size_t)h->plan.padded * dtype_size(h->hp.grad_dtype));
   const size_t xb = round4k((size_t)h->plan.P * (1 + 2 * (size_t)h->plan.nsplit) * sizeof(double));
@@ -209,10 +211,12 @@ static lars_status_t setup_fused(lars_ctx* h) {
   NCCL_OR(ncclCommWindowRegister(h->comm, f.w, wb, &f.wwin, NCCL_WIN_COLL_SYMMETRIC));
   NCCL_OR(ncclCommWindowRegister(h->comm, f.g, gb, &f.gwin, NCCL_WIN_COLL_SYMMETRIC));
   NCCL_OR(ncclCommWindowRegister(h->comm, f.x, xb, &f.xwin, NCCL_WIN_COLL_SYMMETRIC));
-  f.grid = h->sms * kCtasPerSm;  // one resident wave, identical on every rank (per-CTA barriers pair up)
+  // one resident wave each, identical on every rank (the per-CTA barriers pair CTA b with CTA b)
+  f.grid_norm = h->sms * dp_norm_ctas_per_sm(h->plan.P);
+  f.grid_update = h->sms * kCtasPerSm;
   ncclDevCommRequirements reqs;
   std::memset(&reqs, 0, sizeof reqs);
-  reqs.lsaBarrierCount = f.grid + 1;
+  reqs.lsaBarrierCount = std::max(f.grid_norm, f.grid_update) + 1;
   NCCL_OR(ncclDevCommCreate(h->comm, &reqs, &f.dc));
   f.dc_ok = true;
   if (cudaMalloc(&f.gred32, (size_t)h->plan.S * sizeof(float)) != cudaSuccess) return LARS_ERR_OOM;
@@ -444,14 +448,18 @@ lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, cons
   cudaFree(d);
   if (r[0] != h->plan.hash || r[1] != h->plan.hash) return LARS_ERR_LAYOUT;
   const int32_t min_tile = h->hp.tile_elems > 0 ? h->hp.tile_elems : kDefaultMinTile;
-  h->shard.wl = make_worklist(h->plan, rank, h->sms * kCtasPerSm * kTilesPerCta, min_tile);
+  const bool fused = fused_eligible(h);
+  h->shard.wl = make_worklist(h->plan, rank, h->sms * (fused ? dp_norm_ctas_per_sm(nranks) : kCtasPerSm) * kTilesPerCta,
+                              min_tile);
   lars_status_t st = upload(h->shard, h->sms, h->plan.nsplit, true);
   if (st != LARS_OK) return st;
   if (cudaMalloc(&h->gred, (size_t)h->plan.S * dtype_size(h->hp.grad_dtype)) != cudaSuccess) return LARS_ERR_OOM;
   CUDA_OR(cudaMemset(h->gred, 0, (size_t)h->plan.S * dtype_size(h->hp.grad_dtype)));
   h->shard_ready = true;
-  st = setup_fused(h);
-  if (st != LARS_OK) return st;
+  if (fused) {
+    st = setup_fused(h);
+    if (st != LARS_OK) return st;
+  }
   return LARS_OK;
 }
 
@@ -468,7 +476,8 @@ static lars_status_t dp_impl(lars_handle_t h, float* w, const void* g, float* m,
     DpFused f{h->fused.dc, h->fused.gwin, h->fused.wwin, h->fused.xwin, h->rank, h->plan.P, begin, h->fused.gred32};
     prof_rec(pe, 0, s);
     prof_rec(pe, 1, s);
-    CUDA_OR(launch_dp_fused(dt, h->shard.dw, h->shard.sc, hy, w, m, f, h->fused.grid, s, pe ? (*pe)[2] : nullptr,
+    CUDA_OR(launch_dp_fused(dt, h->shard.dw, h->shard.sc, hy, w, m, f, h->fused.grid_norm, h->fused.grid_update, s,
+                            pe ? (*pe)[2] : nullptr,
                             pe ? (*pe)[3] : nullptr));
     if (pe) {
       cudaEventRecord((*pe)[4], s);
