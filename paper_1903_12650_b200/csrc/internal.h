@@ -157,6 +157,9 @@ struct DpFused {
   int rank, nranks;
   int64_t begin;                  // first element of this rank's shard
   float* gred;                    // fp32 reduced shard (S elements)
+  unsigned long long* epoch;      // local step counter (advanced by F1's final CTA)
+  int64_t* step_iter;             // the iteration of the current step, recorded by F1
+  bool mcast;                     // NVLS multicast all-gather (multimem.st) instead of per-peer stores
 };
 // F1 (reduce + norms, grid_norm CTAs), FX (exchange + finish), F2 (update + gather, grid_update CTAs);
 // both grids identical on every rank (the per-CTA LSA barriers pair CTA b with CTA b of every rank).

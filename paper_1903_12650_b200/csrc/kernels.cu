@@ -426,8 +426,10 @@ __device__ __forceinline__ int32_t take_ticket(unsigned long long* t, int32_t ni
 // K1 body, shared by the single-GPU / NCCL kernel and the fused data-parallel kernel (they differ only
 // in where the gradient comes from). Persistent schedule: static (CTA b owns tiles b, b + grid, ...) or
 // dynamic (kNormDynamic).
+// Returns true on thread 0 of the CTA that completed the step's layer count (data-parallel mode: the
+// caller then publishes this rank's C3 shares).
 template <bool CARRY, class GL>
-__device__ __forceinline__ void norms_body(const DevWork& wk, const DevScratch& sc, const Hyper& hy,
+__device__ __forceinline__ bool norms_body(const DevWork& wk, const DevScratch& sc, const Hyper& hy,
                                            const float* __restrict__ w, const GL& gl) {
   __shared__ double sm_cw[kMaxTileChunks], sm_cg[kMaxTileChunks];
   __shared__ unsigned sm_done, sm_nonfinite;
@@ -471,7 +473,7 @@ __device__ __forceinline__ void norms_body(const DevWork& wk, const DevScratch& 
       *(volatile unsigned*)sc.tensors_done = 0u;
       if (sc.c3) {  // data parallel: the decision is global, taken after the C3 exchange
         *(volatile double*)sc.c3 = nf ? 1.0 : 0.0;
-        return;
+        return true;
       }
       int32_t status = nf ? 1 : 0;
       if (hy.iter_dev) {  // every layer has read the iteration: advance it (graph replays walk the schedule)
@@ -480,8 +482,10 @@ __device__ __forceinline__ void norms_body(const DevWork& wk, const DevScratch& 
         *(volatile int64_t*)hy.iter_dev = t + 1;
       }
       *(volatile int32_t*)sc.skip = status;
+      return true;
     }
   }
+  return false;
 }
 
 template <int DT, bool CARRY>
@@ -530,6 +534,22 @@ struct PeerWeights {
   }
   __device__ __forceinline__ void store1(int64_t e, float x) const {
     for (int p = 0; p < n; ++p) pw[p][e] = x;
+  }
+};
+
+// NVLS: one multicast store per vector reaches every rank's weight buffer (the NVSwitch replicates it), so
+// the SM issues 1x the bytes instead of (P-1)x. multimem.st is at most 128-bit.
+struct McastWeights {
+  float* mc;  // multicast address of the weight window (ncclGetLsaMultimemPointer)
+  __device__ __forceinline__ void store8(int64_t e, const F8& x) const {
+    float* d = mc + e;
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(d), "f"(x.v[0]), "f"(x.v[1]),
+                 "f"(x.v[2]), "f"(x.v[3]) : "memory");
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(d + 4), "f"(x.v[4]), "f"(x.v[5]),
+                 "f"(x.v[6]), "f"(x.v[7]) : "memory");
+  }
+  __device__ __forceinline__ void store1(int64_t e, float x) const {
+    asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(mc + e), "f"(x) : "memory");
   }
 };
 
@@ -666,12 +686,70 @@ __global__ void lars_split_finish_kernel(DevWork wk, DevScratch sc, Hyper hy) { 
 // Gradient and weight buffers live in NCCL symmetric windows (ncclMemAlloc + ncclCommWindowRegister), so
 // every rank can load and store every other rank's buffers over NVLink with plain ld/st (LSA pointers).
 // The reduce-scatter is fused into K1 (each rank sums its shard over all ranks' gradients in fp32), the
-// C3 exchange is one warp storing its shares into every peer, and the all-gather is fused into K2 (each
+// C3 exchange rides on F1's tail and F2's head (flagged slots, no extra kernel), and the all-gather is fused into K2 (each
 // updated weight is stored locally and into every peer). Per-CTA LSA barriers order the phases.
 //
-//   F1 lars_dp_reduce_norms_kernel : barrier(b) -> shard sum over ranks + norms (+ split shares)
-//   FX lars_dp_exchange_kernel     : C3 shares -> every peer, barrier, fixed-order sum, finish, skip
-//   F2 lars_dp_update_gather_kernel: update + store w to every peer -> barrier(b)
+//   F1 lars_dp_reduce_norms_kernel : barrier(b) -> shard sum over ranks + norms; the final CTA publishes
+//                                    this rank's C3 shares into every rank's exchange slot (epoch-flagged)
+//   F2 lars_dp_update_gather_kernel: wait for all ranks' shares, fixed-order sum, finish split layers, skip
+//                                    -> update + store w to every peer -> barrier(b)
+// End of F1 (one thread): this rank's C3 shares [non-finite flag, split-layer sums] go into slot [rank] of
+// every rank's exchange window, then the slot's epoch word is released. The iteration of this step is
+// recorded (and a device iteration advanced) here, after every layer of this rank has read it.
+__device__ void dp_publish_shares(const DevWork& wk, const DevScratch& sc, const Hyper& hy, const DpFused& f) {
+  const int32_t n = 1 + 2 * wk.nsplit_total;
+  const unsigned long long epoch = *f.epoch + 1ull;
+  *f.epoch = epoch;
+  const int64_t t = hy.iter_dev ? *(volatile int64_t*)hy.iter_dev : hy.iter;
+  *f.step_iter = t;
+  if (hy.iter_dev) *(volatile int64_t*)hy.iter_dev = t + 1;
+  for (int p = 0; p < f.nranks; ++p) {
+    double* slot = (double*)ncclGetLsaPointer(f.xwin, (size_t)f.rank * (n + 1) * sizeof(double), p);
+    for (int32_t i = 0; i < n; ++i) slot[1 + i] = sc.c3[i];
+    __threadfence_system();
+    cuda::atomic_ref<unsigned long long, cuda::thread_scope_system> flag(*(unsigned long long*)slot);
+    flag.store(epoch, cuda::memory_order_release);
+  }
+  for (int32_t i = 0; i < n; ++i) sc.c3[i] = 0.0;  // next step's shares start from zero
+}
+
+// Start of F2 (warp 0 of every CTA): wait for every rank's shares of this step, sum them in rank order
+// (identical on every rank), finish the split layers this rank touches, decide the skip. Returns the
+// step status (0 apply, 1 non-finite, 2 iteration out of range) to every lane of warp 0.
+__device__ int32_t dp_collect_shares(const DevWork& wk, const DevScratch& sc, const Hyper& hy, const DpFused& f) {
+  const int lane = threadIdx.x & 31;
+  const int32_t n = 1 + 2 * wk.nsplit_total;
+  const unsigned long long epoch = *(volatile unsigned long long*)f.epoch;
+  const double* x = (const double*)ncclGetLocalPointer(f.xwin, 0);
+  if (lane < f.nranks) {
+    cuda::atomic_ref<const unsigned long long, cuda::thread_scope_system> flag(
+        *(const unsigned long long*)(x + (size_t)lane * (n + 1)));
+    while (flag.load(cuda::memory_order_acquire) < epoch) __nanosleep(64);
+  }
+  __syncwarp();
+  bool bad = false;
+  for (int32_t i = lane; i < n; i += 32) {
+    double tot = 0.0;
+    for (int p = 0; p < f.nranks; ++p) tot += x[(size_t)p * (n + 1) + 1 + i];  // rank order
+    bad |= (i == 0) ? (tot > 0.0) : !isfinite(tot);
+  }
+  Hyper h2 = hy;  // the step's iteration as recorded by F1 (a device iteration has moved on already)
+  h2.iter = *(volatile const int64_t*)f.step_iter;
+  h2.iter_dev = nullptr;
+  for (int32_t k = lane; k < wk.nsplit_local; k += 32) {
+    const int32_t l = wk.split_locals[k], j = wk.tsplit[l];
+    double sw = 0.0, sg = 0.0;
+    for (int p = 0; p < f.nranks; ++p) {
+      sw += x[(size_t)p * (n + 1) + 2 + 2 * j];
+      sg += x[(size_t)p * (n + 1) + 3 + 2 * j];
+    }
+    bad |= finish_core(l, sw, sg, wk, sc, h2);  // identical values from every CTA (benign duplicate stores)
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  const bool out_of_range = h2.iter < 0 || h2.iter >= hy.total_iters;
+  return out_of_range ? 2 : bad ? 1 : 0;
+}
+
 template <int DT, bool CARRY, int NP>
 __global__ void __launch_bounds__(kThreads, dp_norm_ctas_per_sm(NP)) lars_dp_reduce_norms_kernel(DevWork wk, DevScratch sc,
                                                                                     Hyper hy, const float* w,
@@ -686,42 +764,39 @@ __global__ void __launch_bounds__(kThreads, dp_norm_ctas_per_sm(NP)) lars_dp_red
   gl.nranks = f.nranks;
   gl.gred = f.gred;
   gl.begin = f.begin;
-  norms_body<CARRY>(wk, sc, hy, w, gl);
+  const bool final_cta = norms_body<CARRY>(wk, sc, hy, w, gl);
+  if (final_cta || (wk.ntensors == 0 && blockIdx.x == 0 && threadIdx.x == 0)) dp_publish_shares(wk, sc, hy, f);
 }
 
-__global__ void lars_dp_exchange_kernel(DevWork wk, DevScratch sc, Hyper hy, DpFused f, int barrier_index) {
-  const int lane = threadIdx.x;
-  const int32_t n = 1 + 2 * wk.nsplit_total;
-  for (int p = 0; p < f.nranks; ++p) {  // my shares into slot [rank] of every rank (myself included)
-    double* dst = (double*)ncclGetLsaPointer(f.xwin, (size_t)f.rank * n * sizeof(double), p);
-    for (int32_t i = lane; i < n; i += 32) dst[i] = sc.c3[i];
-  }
-  {
-    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), f.dc, ncclTeamTagLsa(), barrier_index);
-    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
-  }
-  const double* x = (const double*)ncclGetLocalPointer(f.xwin, 0);
-  for (int32_t i = lane; i < n; i += 32) {
-    double t = 0.0;
-    for (int p = 0; p < f.nranks; ++p) t += x[(size_t)p * n + i];  // rank order: identical everywhere
-    sc.c3[i] = t;
-  }
-  __syncwarp();
-  split_finish_body(wk, sc, hy);
-}
-
-template <bool CARRY>
+template <bool CARRY, bool MCAST>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_dp_update_gather_kernel(DevWork wk, DevScratch sc,
                                                                                      Hyper hy, float* w, float* m,
                                                                                      DpFused f) {
-  const bool skip = *(volatile const int32_t*)sc.skip != 0;
-  PeerWeights ws;
-  ws.n = 0;
-  for (int p = 0; p < f.nranks; ++p)
-    if (p != f.rank) ws.pw[ws.n++] = (float*)ncclGetLsaPointer(f.wwin, 0, p);
-  if (!skip)  // items ordered last-part-of-every-tile first (see update_item), striped over this grid
-    for (int32_t item = blockIdx.x; item < wk.ntiles * kUpdateSplit; item += gridDim.x)
-      update_item<LARS_F32, CARRY, PeerWeights>(item, wk, sc, hy, w, f.gred, f.begin, m, ws);
+  __shared__ int32_t s_status;
+  if (threadIdx.x < 32) {
+    const int32_t st = dp_collect_shares(wk, sc, hy, f);
+    if (threadIdx.x == 0) {
+      s_status = st;
+      if (blockIdx.x == 0) *(volatile int32_t*)sc.skip = st;
+    }
+  }
+  __syncthreads();
+  const bool skip = s_status != 0;
+  if (!skip) {  // items ordered last-part-of-every-tile first (see update_item), striped over this grid
+    if (MCAST) {
+      const McastWeights ws{(float*)ncclGetLsaMultimemPointer(f.wwin, 0, f.dc)};
+      for (int32_t item = blockIdx.x; item < wk.ntiles * kUpdateSplit; item += gridDim.x)
+        update_item<LARS_F32, CARRY, McastWeights>(item, wk, sc, hy, w, f.gred, f.begin, m, ws);
+    } else {
+      PeerWeights ws;
+      ws.n = 0;
+      for (int p = 0; p < f.nranks; ++p)
+        if (p != f.rank) ws.pw[ws.n++] = (float*)ncclGetLsaPointer(f.wwin, 0, p);
+      for (int32_t item = blockIdx.x; item < wk.ntiles * kUpdateSplit; item += gridDim.x)
+        update_item<LARS_F32, CARRY, PeerWeights>(item, wk, sc, hy, w, f.gred, f.begin, m, ws);
+    }
+  }
+  if (MCAST) asm volatile("fence.acq_rel.sys;" ::: "memory");  // multicast stores before the barrier release
   if (CARRY && !skip && blockIdx.x == 0 && threadIdx.x == 0) *(volatile int32_t*)sc.wnext_valid = 1;
   {  // CTA b of every rank has stored its weights => after this grid, every rank's w is complete
     ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), f.dc, ncclTeamTagLsa(), blockIdx.x);
@@ -760,12 +835,14 @@ cudaError_t launch_dp_fused(int32_t dt, const DevWork& wk, const DevScratch& sc,
   wg.grid = grid_norm;
   launch_reduce_norms(dt, hy.carry, f.nranks, grid_norm, st, wg, sc, hy, w, f);
   if (ev1) cudaEventRecord(ev1, st);
-  lars_dp_exchange_kernel<<<1, 32, 0, st>>>(wg, sc, hy, f, grid_update);
-  if (ev2) cudaEventRecord(ev2, st);
-  if (hy.carry)
-    lars_dp_update_gather_kernel<true><<<grid_update, kThreads, 0, st>>>(wg, sc, hy, w, m, f);
-  else
-    lars_dp_update_gather_kernel<false><<<grid_update, kThreads, 0, st>>>(wg, sc, hy, w, m, f);
+  if (ev2) cudaEventRecord(ev2, st);  // (the exchange now lives inside F1's tail and F2's head)
+  if (hy.carry) {
+    if (f.mcast) lars_dp_update_gather_kernel<true, true><<<grid_update, kThreads, 0, st>>>(wg, sc, hy, w, m, f);
+    else lars_dp_update_gather_kernel<true, false><<<grid_update, kThreads, 0, st>>>(wg, sc, hy, w, m, f);
+  } else {
+    if (f.mcast) lars_dp_update_gather_kernel<false, true><<<grid_update, kThreads, 0, st>>>(wg, sc, hy, w, m, f);
+    else lars_dp_update_gather_kernel<false, false><<<grid_update, kThreads, 0, st>>>(wg, sc, hy, w, m, f);
+  }
   return cudaGetLastError();
 }
 

@@ -173,7 +173,9 @@ struct lars_ctx {
     ncclDevComm dc{};
     bool dc_ok = false;
     float* gred32 = nullptr;
+    void* state = nullptr;  // epoch + step iteration
     int grid_norm = 0, grid_update = 0;
+    bool mcast = false;
   } fused;
   int32_t last_red_dtype = LARS_F16;
   const void* last_red = nullptr;
@@ -201,7 +203,8 @@ static bool fused_eligible(lars_ctx* h) {
 static lars_status_t setup_fused(lars_ctx* h) {
   auto& f = h->fused;
   const size_t wb = round4k((size_t)h->plan.padded * 4), gb = round4k((size_t)h->plan.padded * dtype_size(h->hp.grad_dtype));
-  const size_t xb = round4k((size_t)h->plan.P * (1 + 2 * (size_t)h->plan.nsplit) * sizeof(double));
+  // exchange slot per rank: [epoch | non-finite flag | split-layer sums]
+  const size_t xb = round4k((size_t)h->plan.P * (2 + 2 * (size_t)h->plan.nsplit) * sizeof(double));
   NCCL_OR(ncclMemAlloc(&f.w, wb));
   NCCL_OR(ncclMemAlloc(&f.g, gb));
   NCCL_OR(ncclMemAlloc(&f.x, xb));
@@ -217,9 +220,19 @@ static lars_status_t setup_fused(lars_ctx* h) {
   ncclDevCommRequirements reqs;
   std::memset(&reqs, 0, sizeof reqs);
   reqs.lsaBarrierCount = std::max(f.grid_norm, f.grid_update) + 1;
-  NCCL_OR(ncclDevCommCreate(h->comm, &reqs, &f.dc));
+  // NVLS multicast all-gather (multimem.st) is opt-in: measured 2x slower than per-peer stores for fp32
+  // weights on B200 (profiles/README.md), so per-peer NVLink stores are the default.
+  const char* mc_env = getenv("LARS_DP_MCAST");
+  reqs.lsaMultimem = mc_env && mc_env[0] == '1';
+  if (ncclDevCommCreate(h->comm, &reqs, &f.dc) != ncclSuccess) {
+    reqs.lsaMultimem = false;
+    NCCL_OR(ncclDevCommCreate(h->comm, &reqs, &f.dc));
+  }
+  f.mcast = reqs.lsaMultimem;
   f.dc_ok = true;
   if (cudaMalloc(&f.gred32, (size_t)h->plan.S * sizeof(float)) != cudaSuccess) return LARS_ERR_OOM;
+  if (cudaMalloc(&f.state, 64) != cudaSuccess) return LARS_ERR_OOM;
+  CUDA_OR(cudaMemset(f.state, 0, 64));
   CUDA_OR(cudaMemset(f.gred32, 0, (size_t)h->plan.S * sizeof(float)));
   CUDA_OR(cudaDeviceSynchronize());
   f.ok = true;
@@ -473,7 +486,9 @@ static lars_status_t dp_impl(lars_handle_t h, float* w, const void* g, float* m,
   if (cg != LARS_OK) return cg;
   auto* pe = h->prof.begin(2);
   if (h->fused.ok && (void*)w == h->fused.w && g == h->fused.g) {  // fused NVLink path (F1, FX, F2)
-    DpFused f{h->fused.dc, h->fused.gwin, h->fused.wwin, h->fused.xwin, h->rank, h->plan.P, begin, h->fused.gred32};
+    DpFused f{h->fused.dc,   h->fused.gwin, h->fused.wwin,  h->fused.xwin,
+              h->rank,       h->plan.P,     begin,          h->fused.gred32,
+              (unsigned long long*)h->fused.state, (int64_t*)((char*)h->fused.state + 8), h->fused.mcast};
     prof_rec(pe, 0, s);
     prof_rec(pe, 1, s);
     CUDA_OR(launch_dp_fused(dt, h->shard.dw, h->shard.sc, hy, w, m, f, h->fused.grid_norm, h->fused.grid_update, s,
@@ -688,6 +703,7 @@ lars_status_t lars_destroy(lars_handle_t h) {
       if (f.g) ncclMemFree(f.g);
       if (f.x) ncclMemFree(f.x);
       cudaFree(f.gred32);
+      cudaFree(f.state);
       ncclCommDestroy(h->comm);
     }
     cudaFree(h->lr_d);
