@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--layout", default="resnet50")
     ap.add_argument("--no-fused", action="store_true",
                     help="P > 1: use the NCCL collective path instead of the fused NVLink kernels")
+    ap.add_argument("--buckets", type=int, default=0, help="NCCL path: K tile-aligned buckets (0/1 = single shot)")
     ap.add_argument("--no-carry", action="store_true",
                     help="disable LARS_FLAG_CARRY_WNORM (K2 carries sum(w^2) so K1 reads only g)")
     return ap.parse_args()
@@ -138,7 +139,7 @@ def run_ours(args):
     E = sum(t.numel for t in lay)
     carry = not args.no_carry
     mk = lambda flags: PK.Lars([(t.numel, t.kind) for t in lay], device=local, grad_dtype=dtype, nranks=P,
-                               grad_scale=1.0 / (G.GRAD_PRESCALE * P), flags=flags, **HP)
+                               grad_scale=1.0 / (G.GRAD_PRESCALE * P), flags=flags, buckets=args.buckets, **HP)
     h = mk(PK.lars.FLAG_CARRY_WNORM if carry else 0)
     if P > 1:
         h.comm_init_torch()
@@ -300,6 +301,7 @@ def run_ours(args):
                    "params": E, "global_batch": HP["global_batch"], "iters": f"t=({T0}+k) mod {T}",
                    "parallelism": f"dp{P}", "units": f"{P} x {E} gradient params combined+applied per step",
                    "dp_path": None if P == 1 else ("fused-nvlink" if fused else "nccl"),
+                   "nccl_buckets": args.buckets if P > 1 else None,
                    "l2": f"inputs larger than L2: w+g+m = {(8 + gbytes) * h.padded_numel / 1e6:.0f} MB > 126 MB, "
                          "no flush"},
         "phases_ms": {kk: round(v, 5) for kk, v in ph.items() if v > 0},

@@ -100,6 +100,12 @@ typedef struct {
   int32_t tile_elems;    /* minimum work-tile size in elements; 0 = library default                */
   int32_t shard_policy;  /* lars_shard_policy_t (default LARS_SHARD_CONTIGUOUS)                    */
   uint32_t flags;        /* LARS_FLAG_* (default 0)                                               */
+  int32_t buckets;       /* NCCL path, P > 1: K >= 2 splits every shard into K tile-aligned buckets;
+                            reduce-scatter bucket k (grouped ncclReduce, one per root) overlaps the
+                            norms of bucket k-1, and the update of bucket k overlaps the weight
+                            broadcast of bucket k-1 ("several megabytes"). 0/1 =
+                            one ncclReduceScatter + one ncclAllGather (default)                    */
+  int32_t reserved;      /* must be 0                                                             */
 } lars_hparams_t;
 
 /* Carry the weight norms: K2 also produces sum(w_new^2) for every layer, so the next step's K1 reads only

@@ -179,7 +179,57 @@ struct lars_ctx {
   } fused;
   int32_t last_red_dtype = LARS_F16;
   const void* last_red = nullptr;
+  // bucketed NCCL schedule (hp.buckets = K >= 2): bucket k of rank r covers shard-relative elements
+  // [bucket_elem[r*(K+1)+k], bucket_elem[r*(K+1)+k+1]) = this rank's tiles [bucket_tile[k], bucket_tile[k+1])
+  int32_t K = 1;
+  std::vector<int64_t> bucket_elem;
+  std::vector<int32_t> bucket_tile;
+  cudaStream_t cs = nullptr;  // communication stream of the bucketed schedule
+  std::vector<cudaEvent_t> ev;
 };
+
+// Tile-aligned buckets of ~equal element counts for every rank (the plan is static: every rank derives
+// every other rank's boundaries without communication).
+static void make_buckets(lars_ctx* h, int32_t ntiles_target, int32_t min_tile) {
+  const int32_t K = h->K, P = h->plan.P;
+  h->bucket_elem.assign((size_t)P * (K + 1), 0);
+  for (int32_t r = 0; r < P; ++r) {
+    const WorkList wl = r == h->rank ? h->shard.wl : make_worklist(h->plan, r, ntiles_target, min_tile);
+    const int32_t nt = wl.ntiles();
+    std::vector<int64_t> tile_elems(nt, 0);
+    int64_t total = 0;
+    for (int32_t t = 0; t < nt; ++t) {
+      for (int32_t sgi = wl.tile_seg[t]; sgi < wl.tile_seg[t + 1]; ++sgi) tile_elems[t] += wl.segs[sgi].len;
+      total += tile_elems[t];
+    }
+    std::vector<int32_t> tb(K + 1, nt);
+    tb[0] = 0;
+    int64_t acc = 0;
+    int32_t k = 1;
+    for (int32_t t = 0; t < nt && k < K; ++t) {
+      acc += tile_elems[t];
+      while (k < K && acc * K >= total * k) tb[k++] = t + 1;
+    }
+    int64_t* eb = &h->bucket_elem[(size_t)r * (K + 1)];
+    for (int32_t kk = 0; kk <= K; ++kk) {
+      if (kk == 0) eb[kk] = 0;
+      else if (kk == K || tb[kk] >= nt) eb[kk] = h->plan.S;
+      else eb[kk] = wl.segs[wl.tile_seg[tb[kk]]].begin - (int64_t)r * h->plan.S;
+    }
+    for (int32_t kk = 1; kk <= K; ++kk) eb[kk] = std::max(eb[kk], eb[kk - 1]);
+    if (r == h->rank) h->bucket_tile = tb;
+  }
+}
+
+// A contiguous tile range of a work list as its own launchable work list (device pointers offset).
+static DevWork sub_work(const DevWork& w, int32_t t0, int32_t t1) {
+  DevWork s = w;
+  s.tile_seg = w.tile_seg + t0;
+  s.tile_chunk = w.tile_chunk + t0;
+  s.ntiles = t1 - t0;
+  s.grid = t1 - t0;
+  return s;
+}
 
 #define CUDA_OR(expr)                                      \
   do {                                                     \
@@ -462,8 +512,15 @@ lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, cons
   if (r[0] != h->plan.hash || r[1] != h->plan.hash) return LARS_ERR_LAYOUT;
   const int32_t min_tile = h->hp.tile_elems > 0 ? h->hp.tile_elems : kDefaultMinTile;
   const bool fused = fused_eligible(h);
-  h->shard.wl = make_worklist(h->plan, rank, h->sms * (fused ? dp_norm_ctas_per_sm(nranks) : kCtasPerSm) * kTilesPerCta,
-                              min_tile);
+  const int32_t ntiles_target = h->sms * (fused ? dp_norm_ctas_per_sm(nranks) : kCtasPerSm) * kTilesPerCta;
+  h->shard.wl = make_worklist(h->plan, rank, ntiles_target, min_tile);
+  h->K = std::max(1, h->hp.buckets);
+  if (h->K > 1) {
+    make_buckets(h, ntiles_target, min_tile);
+    CUDA_OR(cudaStreamCreateWithFlags(&h->cs, cudaStreamNonBlocking));
+    h->ev.resize(2 * (size_t)h->K + 2, nullptr);
+    for (auto& e : h->ev) CUDA_OR(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   lars_status_t st = upload(h->shard, h->sms, h->plan.nsplit, true);
   if (st != LARS_OK) return st;
   if (cudaMalloc(&h->gred, (size_t)h->plan.S * dtype_size(h->hp.grad_dtype)) != cudaSuccess) return LARS_ERR_OOM;
@@ -473,6 +530,70 @@ lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, cons
     st = setup_fused(h);
     if (st != LARS_OK) return st;
   }
+  return LARS_OK;
+}
+
+// Bucketed NCCL schedule. Communication stream cs: RS(0..K-1) as grouped ncclReduce (one per root rank,
+// each rank receiving its own bucket k), then the weight broadcasts. Compute stream s: K1(bucket k) after
+// RS(k); C3 + finisher; K2(bucket k) -> broadcast(bucket k) on cs. The per-layer finishing of K1 spans the
+// K launches (its counters persist), so results are identical to K = 1 up to NCCL's reduction order.
+static lars_status_t dp_bucketed(lars_handle_t h, float* w, const void* g, float* m, const Hyper& hy, cudaStream_t s,
+                                 std::array<cudaEvent_t, 6>* pe) {
+  const int32_t K = h->K, P = h->plan.P, dt = h->hp.grad_dtype, me = h->rank;
+  const int64_t S = h->plan.S, begin = (int64_t)me * S;
+  const size_t esz = dtype_size(dt);
+  cudaEvent_t* ev_rs = &h->ev[0];
+  cudaEvent_t* ev_k2 = &h->ev[K];
+  cudaEvent_t ev_go = h->ev[2 * K], ev_done = h->ev[2 * K + 1];
+  const DevWork& wk = h->shard.dw;
+  const int32_t* tb = h->bucket_tile.data();
+  prof_rec(pe, 0, s);
+  CUDA_OR(cudaEventRecord(ev_go, s));  // the caller's gradient is ready
+  CUDA_OR(cudaStreamWaitEvent(h->cs, ev_go, 0));
+  for (int32_t k = 0; k < K; ++k) {  // C1 in K buckets
+    NCCL_OR(ncclGroupStart());
+    for (int32_t r = 0; r < P; ++r) {
+      const int64_t* eb = &h->bucket_elem[(size_t)r * (K + 1)];
+      const size_t cnt = (size_t)(eb[k + 1] - eb[k]);
+      if (!cnt) continue;
+      NCCL_OR(ncclReduce((const char*)g + ((int64_t)r * S + eb[k]) * esz, (char*)h->gred + eb[k] * esz, cnt,
+                         nccl_type(dt), ncclSum, r, h->comm, h->cs));
+    }
+    NCCL_OR(ncclGroupEnd());
+    CUDA_OR(cudaEventRecord(ev_rs[k], h->cs));
+  }
+  for (int32_t k = 0; k < K; ++k) {  // K1 of bucket k as soon as its sums have landed
+    CUDA_OR(cudaStreamWaitEvent(s, ev_rs[k], 0));
+    if (tb[k + 1] > tb[k]) CUDA_OR(launch_norms(dt, sub_work(wk, tb[k], tb[k + 1]), h->shard.sc, hy, w, h->gred, begin, s));
+  }
+  prof_rec(pe, 1, s);
+  prof_rec(pe, 2, s);
+  NCCL_OR(ncclAllReduce(h->shard.sc.c3, h->shard.sc.c3, 1 + 2 * (size_t)h->plan.nsplit, ncclFloat64, ncclSum,
+                        h->comm, s));                                                             // C3
+  CUDA_OR(launch_split_finish(wk, h->shard.sc, hy, s));
+  prof_rec(pe, 3, s);
+  for (int32_t k = 0; k < K; ++k) {  // K2 of bucket k, then its weights go out while K2 of k+1 runs
+    if (tb[k + 1] > tb[k]) CUDA_OR(launch_update(dt, sub_work(wk, tb[k], tb[k + 1]), h->shard.sc, hy, w, h->gred, begin, m, s));
+    CUDA_OR(cudaEventRecord(ev_k2[k], s));
+    CUDA_OR(cudaStreamWaitEvent(h->cs, ev_k2[k], 0));
+    NCCL_OR(ncclGroupStart());
+    for (int32_t r = 0; r < P; ++r) {  // C2: rank r broadcasts its bucket k to everyone (in place)
+      const int64_t* eb = &h->bucket_elem[(size_t)r * (K + 1)];
+      const size_t cnt = (size_t)(eb[k + 1] - eb[k]);
+      if (!cnt) continue;
+      float* p = w + (int64_t)r * S + eb[k];
+      NCCL_OR(ncclBroadcast(p, p, cnt, ncclFloat32, r, h->comm, h->cs));
+    }
+    NCCL_OR(ncclGroupEnd());
+  }
+  CUDA_OR(cudaEventRecord(ev_done, h->cs));
+  CUDA_OR(cudaStreamWaitEvent(s, ev_done, 0));  // the step ends on the caller's stream
+  prof_rec(pe, 4, s);
+  prof_rec(pe, 5, s);
+  h->last_stream = s;
+  h->last = &h->shard;
+  h->last_red = h->gred;
+  h->last_red_dtype = dt;
   return LARS_OK;
 }
 
@@ -504,6 +625,7 @@ static lars_status_t dp_impl(lars_handle_t h, float* w, const void* g, float* m,
     h->last_red_dtype = LARS_F32;
     return LARS_OK;
   }
+  if (h->K > 1) return dp_bucketed(h, w, g, m, hy, s, pe);
   prof_rec(pe, 0, s);
   NCCL_OR(ncclReduceScatter(g, h->gred, (size_t)S, nccl_type(dt), ncclSum, h->comm, s));          // C1
   prof_rec(pe, 1, s);
@@ -704,6 +826,9 @@ lars_status_t lars_destroy(lars_handle_t h) {
       if (f.x) ncclMemFree(f.x);
       cudaFree(f.gred32);
       cudaFree(f.state);
+      for (auto e : h->ev)
+        if (e) cudaEventDestroy(e);
+      if (h->cs) cudaStreamDestroy(h->cs);
       ncclCommDestroy(h->comm);
     }
     cudaFree(h->lr_d);

@@ -29,6 +29,7 @@ lars_status_t validate_hparams(const lars_hparams_t& hp) {
   if (hp.grad_dtype < LARS_F32 || hp.grad_dtype > LARS_BF16) return LARS_ERR_INVALID_ARG;
   if (hp.nranks < 1 || hp.nranks > 4096) return LARS_ERR_INVALID_ARG;
   if (hp.tile_elems < 0) return LARS_ERR_INVALID_ARG;
+  if (hp.buckets < 0 || hp.buckets > 1024 || hp.reserved != 0) return LARS_ERR_INVALID_ARG;
   return LARS_OK;
 }
 

@@ -45,7 +45,8 @@ class HParams(ctypes.Structure):
                 ("eps", c_double), ("warmup_epochs", c_double), ("poly_power", c_double),
                 ("grad_scale", c_double), ("global_batch", c_int64), ("dataset_size", c_int64),
                 ("total_epochs", c_int32), ("grad_dtype", c_int32), ("nranks", c_int32),
-                ("tile_elems", c_int32), ("shard_policy", c_int32), ("flags", ctypes.c_uint32)]
+                ("tile_elems", c_int32), ("shard_policy", c_int32), ("flags", ctypes.c_uint32),
+                ("buckets", c_int32), ("reserved", c_int32)]
 
 
 _lib = None

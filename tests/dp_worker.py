@@ -156,6 +156,9 @@ def main():
              ("r50-f16", lay_r50, "f16", 719, {}),
              ("r50-int", lay_r50, "f16", 1439, dict(kind="integer")),
              ("r50-lpt-f16", lay_r50, "f16", 80, dict(shard_policy="lpt")),
+             ("r50-f16-buckets4", lay_r50, "f16", 81, dict(buckets=4)),
+             ("random-bf16-buckets3", LY.random_layout(np.random.default_rng(18), 40), "bf16", 82, dict(buckets=3)),
+             ("r50-int-buckets8-carry", lay_r50, "f16", 83, dict(kind="integer", buckets=8, flags=1)),
              ("zipf-f16", LY.skew1b("zipf", n_tensors=200, total=4_000_000), "f16", 500, {}),
              ("nan-on-rank1", LY.tiny(), "f16", 100, dict(inject_nan=True)),
              ("fused-tiny-int", LY.tiny(), "f16", 80, dict(kind="integer", fused=True)),
