@@ -145,6 +145,10 @@ lars_status_t lars_shard_range(lars_handle_t h, int32_t rank, int64_t* begin, in
  * boundary under LARS_SHARD_CONTIGUOUS is updated piecewise by every rank it touches). */
 lars_status_t lars_tensor_owner(lars_handle_t h, int32_t* owner);
 
+/* Work decomposition of the single-GPU work list (rank < 0) or of a rank's shard: tiles (= CTAs of K1/K2),
+ * segments (pieces of layers inside tiles) and warp chunks. Any output may be NULL. */
+lars_status_t lars_work_info(lars_handle_t h, int32_t rank, int32_t* ntiles, int32_t* nsegs, int32_t* nchunks);
+
 /* 64-bit FNV-1a hash of (layout, hyper-parameters, P); equal on every rank that planned alike. */
 lars_status_t lars_layout_hash(lars_handle_t h, uint64_t* hash);
 

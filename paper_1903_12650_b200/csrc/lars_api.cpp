@@ -400,6 +400,25 @@ lars_status_t lars_tensor_owner(lars_handle_t h, int32_t* owner) {
   return LARS_OK;
 }
 
+lars_status_t lars_work_info(lars_handle_t h, int32_t rank, int32_t* ntiles, int32_t* nsegs, int32_t* nchunks) {
+  if (!h || rank >= h->plan.P) return LARS_ERR_INVALID_ARG;
+  WorkList tmp;
+  const WorkList* wl = &h->full.wl;
+  if (rank >= 0) {
+    if (h->shard_ready && rank == h->rank) {
+      wl = &h->shard.wl;
+    } else {
+      const int32_t min_tile = h->hp.tile_elems > 0 ? h->hp.tile_elems : kDefaultMinTile;
+      tmp = make_worklist(h->plan, rank, h->sms * kCtasPerSm * kTilesPerCta, min_tile);
+      wl = &tmp;
+    }
+  }
+  if (ntiles) *ntiles = wl->ntiles();
+  if (nsegs) *nsegs = (int32_t)wl->segs.size();
+  if (nchunks) *nchunks = (int32_t)wl->chunks.size();
+  return LARS_OK;
+}
+
 lars_status_t lars_layout_hash(lars_handle_t h, uint64_t* hash) {
   if (!h || !hash) return LARS_ERR_INVALID_ARG;
   *hash = h->plan.hash;

@@ -182,14 +182,20 @@ WorkList make_worklist(const Plan& p, int32_t rank, int32_t ntiles_target, int32
     if (hi > lo) cost += (hi - lo) + kSegCost + kChunkCost * ((hi - lo + kChunk - 1) / kChunk);
   }
   ntiles_target = std::max(1, ntiles_target);
-  int64_t target = std::max<int64_t>(min_tile, (cost + ntiles_target - 1) / ntiles_target);
-  WorkList wl;
-  for (int it = 0; it < 64; ++it) {
-    wl = make_worklist_once(p, rank, ntiles_target, target);
-    if (wl.ntiles() <= ntiles_target) break;
-    target += std::max<int64_t>(kAlign, target / 32);
+  // Smallest tile size whose plan fits the tile budget (binary search): one tile per resident CTA keeps
+  // every SM equally loaded (a 512-tile plan on 592 CTA slots leaves 80 SMs a CTA short). When the chunk
+  // cap forces more tiles than CTAs (very large layouts), the budget becomes the next multiple of the CTA
+  // count, so the static round robin still gives every CTA the same number of tiles.
+  const int64_t top = cost + kSegCost + kChunkCost + kAlign;
+  int32_t budget = ntiles_target;
+  while (make_worklist_once(p, rank, budget, top).ntiles() > budget) budget += ntiles_target;
+  int64_t lo = std::max<int64_t>(min_tile, 1) - 1, hi = top;  // plan(hi) fits, plan(lo) is below the search
+  while (hi - lo > kAlign) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (make_worklist_once(p, rank, budget, mid).ntiles() <= budget) hi = mid;
+    else lo = mid;
   }
-  return wl;
+  return make_worklist_once(p, rank, budget, hi);
 }
 
 static WorkList make_worklist_once(const Plan& p, int32_t rank, int32_t ntiles_target, int64_t target) {

@@ -70,6 +70,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "lars_shard_range": (c_int32, [h, c_int32, POINTER(c_int64), POINTER(c_int64)]),
         "lars_tensor_owner": (c_int32, [h, POINTER(c_int32)]),
         "lars_layout_hash": (c_int32, [h, POINTER(c_uint64)]),
+        "lars_work_info": (c_int32, [h, c_int32, POINTER(c_int32), POINTER(c_int32), POINTER(c_int32)]),
         "lars_step": (c_int32, [h, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
         "lars_step_host_grad": (c_int32, [h, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
         "lars_step_dev_iter": (c_int32, [h, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
@@ -203,6 +204,11 @@ class Lars:
         o = (c_int32 * self.n)()
         _check(self._lib.lars_tensor_owner(self._h, o), "lars_tensor_owner")
         return list(o)
+
+    def work_info(self, rank: int = -1) -> dict:
+        t, sg, c = c_int32(), c_int32(), c_int32()
+        _check(self._lib.lars_work_info(self._h, rank, byref(t), byref(sg), byref(c)), "lars_work_info")
+        return {"tiles": t.value, "segments": sg.value, "chunks": c.value}
 
     def layout_hash(self) -> int:
         x = c_uint64()
