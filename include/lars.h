@@ -78,9 +78,9 @@ typedef enum {
 typedef enum { LARS_F32 = 0, LARS_F16 = 1, LARS_BF16 = 2 } lars_dtype_t;
 
 typedef struct {
-  int64_t numel; /* > 0 */
-  int32_t kind;  /* lars_kind_t */
-  int32_t reserved;
+  int64_t numel;  /* > 0 */
+  int32_t kind;   /* lars_kind_t */
+  int32_t fan_in; /* fan-in of a weight-kind layer for lars_init_weights (0: numel); else unused */
 } lars_tensor_t;
 
 typedef struct {
@@ -144,6 +144,16 @@ lars_status_t lars_shard_range(lars_handle_t h, int32_t rank, int64_t* begin, in
 /* owner[n]: the rank whose shard holds each tensor's first element (a layer that straddles a shard
  * boundary under LARS_SHARD_CONTIGUOUS is updated piecewise by every rank it touches). */
 lars_status_t lars_tensor_owner(lars_handle_t h, int32_t* owner);
+
+/* Parallel deterministic initialization (§III-B-1: "every process has the same seed and
+ * initializes weights in parallel ... without the broadcast operation"). Fills every layer of w (device, fp32, lars_layout offsets; padding untouched) on `stream`:
+ *   weight kind: truncated normal in [-2 sigma, 2 sigma], sigma = sqrt(2 / fan_in) ("truncated_normal",
+ *                PAPER.md:268), by inverse CDF: z = sqrt(2) erfinv(2p - 1), p = Phi(-2) + u (1 - 2 Phi(-2));
+ *   BN gamma: 1;  BN beta, bias: 0.
+ * u = (x >> 11) * 2^-53 with x word (i mod 4) of Philox4x64-10(counter = (i / 4, layer, 0, 0),
+ * key = (seed, 0x4C415253)) for element i of layer l: a pure function of (seed, layer, i), so every rank and
+ * every launch configuration produces bitwise the same weights with zero communication. */
+lars_status_t lars_init_weights(lars_handle_t h, float* w, uint64_t seed, void* stream);
 
 /* Work decomposition of the single-GPU work list (rank < 0) or of a rank's shard: tiles (= CTAs of K1/K2),
  * segments (pieces of layers inside tiles) and warp chunks. Any output may be NULL. */

@@ -199,3 +199,54 @@ def update(hp: HParams, lr: float, lam: float, beta: float, w, G, m, abs_g_sum):
 def dp_step(kinds: list, hp: HParams, t: int, w: list, g_ranks: list, m: list) -> StepResult:
     """O8: P simulated ranks. The data-parallel result is O1-O7 with the exact rank sum."""
     return step(kinds, hp, t, w, g_ranks, m)
+
+
+# ----------------------------------------------------------------------------------------------
+# Parallel deterministic initialization (PAPER.md:119-127, §III-B-1; NEXT-f4): "every process has the
+# same seed and initializes weights in parallel" — a counter-based generator makes every weight a pure
+# function of (seed, layer, element), so no broadcast is needed. "truncated_normal" (PAPER.md:268).
+# ----------------------------------------------------------------------------------------------
+PHILOX_M = (0xD2E7470EE14C6C93, 0xCA5A826395121157)
+PHILOX_W = (0x9E3779B97F4A7C15, 0xBB67AE8584CAA73B)
+INIT_KEY1 = 0x4C415253  # "LARS"
+_M64 = (1 << 64) - 1
+
+
+def philox4x64_10(counter, key) -> tuple:
+    """Philox4x64-10 (Salmon et al., SC'11) on one 256-bit counter, Python integers (reference)."""
+    c, k = list(counter), list(key)
+    for r in range(10):
+        if r:
+            k = [(k[0] + PHILOX_W[0]) & _M64, (k[1] + PHILOX_W[1]) & _M64]
+        p0, p1 = PHILOX_M[0] * c[0], PHILOX_M[1] * c[2]
+        c = [(p1 >> 64) ^ c[1] ^ k[0], p1 & _M64, (p0 >> 64) ^ c[3] ^ k[1], p0 & _M64]
+    return tuple(c)
+
+
+def init_uniform(seed: int, layer: int, n: int) -> np.ndarray:
+    """u_i = (x_i >> 11) 2^-53, x_i = word (i mod 4) of Philox4x64-10((i // 4, layer, 0, 0), (seed, "LARS"))."""
+    words = []
+    for blk in range((n + 3) // 4):
+        words.extend(philox4x64_10((blk, layer, 0, 0), (seed & _M64, INIT_KEY1)))
+    x = np.array(words[:n], dtype=np.uint64)
+    return (x >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+
+
+def init_weights(kinds: list, numels: list, fan_ins: list, seed: int) -> list:
+    """Weight kind: sigma * sqrt(2) * erfinv(2p - 1), p = Phi(-2) + u (1 - 2 Phi(-2)), sigma = sqrt(2/fan_in)
+    (truncated at +-2 sigma); BN gamma 1; BN beta and biases 0. Returns float64 arrays."""
+    from scipy.special import erfinv
+
+    phi_m2 = 0.5 * math.erfc(math.sqrt(2.0))  # Phi(-2)
+    out = []
+    for l, (kind, n) in enumerate(zip(kinds, numels)):
+        if kind == WEIGHT:
+            u = init_uniform(seed, l, n)
+            p = phi_m2 + u * (1.0 - 2.0 * phi_m2)
+            sigma = math.sqrt(2.0 / (fan_ins[l] or n))
+            out.append(sigma * (math.sqrt(2.0) * erfinv(2.0 * p - 1.0)))
+        elif kind == BN_GAMMA:
+            out.append(np.ones(n))
+        else:
+            out.append(np.zeros(n))
+    return out

@@ -74,6 +74,7 @@ struct Plan {
   int32_t L = 0, P = 1;
   std::vector<int64_t> numel;
   std::vector<int32_t> kind;
+  std::vector<int32_t> fan_in;  // 0 = numel (parallel initialization only)
   std::vector<int32_t> owner;   // rank holding the tensor's first element
   std::vector<int32_t> split;   // split slot of a tensor straddling shards (-1: whole on its owner)
   int32_t nsplit = 0;
@@ -167,6 +168,15 @@ struct DpFused {
 cudaError_t launch_dp_fused(int32_t grad_dtype, const DevWork& wk, const DevScratch& sc, const Hyper& hy, float* w,
                             float* m, const DpFused& f, int grid_norm, int grid_update, cudaStream_t stream,
                             cudaEvent_t ev1, cudaEvent_t ev2);
+
+// Per-layer table of the parallel initialization (indexed by the work list's local layer id).
+struct InitTable {
+  const int64_t* offset;  // flat offset of the layer
+  const int32_t* layer;   // global layer index (the Philox counter's second word)
+  const int32_t* kind;
+  const double* sigma;    // sqrt(2 / fan_in) for weight-kind layers
+};
+cudaError_t launch_init_weights(const DevWork& wk, const InitTable& it, float* w, uint64_t seed, cudaStream_t stream);
 
 // After the C3 allreduce: finish split layers, decide the global skip, advance a device iteration.
 cudaError_t launch_split_finish(const DevWork& wk, const DevScratch& sc, const Hyper& hy, cudaStream_t stream);

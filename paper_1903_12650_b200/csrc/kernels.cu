@@ -851,6 +851,64 @@ cudaError_t launch_split_finish(const DevWork& wk, const DevScratch& sc, const H
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- parallel deterministic initialization
+// PAPER.md:119-127 (§III-B-1): every rank initializes the weights itself from the same seed — no broadcast.
+// Each weight is a pure function of (seed, layer, element): Philox4x64-10 counter-based random numbers,
+// truncated normal by inverse CDF (no rejection, so no data-dependent stream consumption).
+__device__ __forceinline__ void philox4x64_10(uint64_t c[4], uint64_t k0, uint64_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += 0x9E3779B97F4A7C15ull;
+      k1 += 0xBB67AE8584CAA73Bull;
+    }
+    const uint64_t lo0 = 0xD2E7470EE14C6C93ull * c[0], hi0 = __umul64hi(0xD2E7470EE14C6C93ull, c[0]);
+    const uint64_t lo1 = 0xCA5A826395121157ull * c[2], hi1 = __umul64hi(0xCA5A826395121157ull, c[2]);
+    const uint64_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) lars_init_weights_kernel(DevWork wk, InitTable it, float* __restrict__ w,
+                                                                    uint64_t seed) {
+  constexpr int kWarps = kThreads / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double phi_m2 = 0.022750131948179195;  // Phi(-2) = erfc(sqrt 2) / 2
+  for (int32_t tile = blockIdx.x; tile < wk.ntiles; tile += gridDim.x) {
+    const int32_t c0 = wk.tile_chunk[tile], c1 = wk.tile_chunk[tile + 1];
+    for (int32_t c = c0 + warp; c < c1; c += kWarps) {
+      const Seg ck = wk.chunks[c];
+      const int32_t l = ck.tensor;
+      const int32_t kind = it.kind[l];
+      const int64_t i0 = ck.begin - it.offset[l];  // element index inside the layer (multiple of 4)
+      for (int32_t q = 4 * lane; q < ck.len; q += 128) {
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        if (kind == LARS_KIND_WEIGHT) {
+          uint64_t x[4] = {(uint64_t)(i0 + q) >> 2, (uint64_t)it.layer[l], 0ull, 0ull};
+          philox4x64_10(x, seed, 0x4C415253ull);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const double u = (double)(x[k] >> 11) * 0x1.0p-53;
+            const double p = phi_m2 + u * (1.0 - 2.0 * phi_m2);
+            v[k] = (float)(it.sigma[l] * (1.4142135623730951 * erfinv(2.0 * p - 1.0)));
+          }
+        } else if (kind == LARS_KIND_BN_GAMMA) {
+          v[0] = v[1] = v[2] = v[3] = 1.f;
+        }
+        for (int k = 0; k < 4 && q + k < ck.len; ++k) w[ck.begin + q + k] = v[k];
+      }
+    }
+  }
+}
+
+cudaError_t launch_init_weights(const DevWork& wk, const InitTable& it, float* w, uint64_t seed, cudaStream_t st) {
+  lars_init_weights_kernel<<<wk.grid, kThreads, 0, st>>>(wk, it, w, seed);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- launchers
 template <typename K, typename... Args>
 static cudaError_t launch_pdl(K kernel, int grid, cudaStream_t stream, Args... args) {

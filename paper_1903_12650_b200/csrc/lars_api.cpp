@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <array>
+#include <cmath>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -186,6 +187,8 @@ struct lars_ctx {
   std::vector<int32_t> bucket_tile;
   cudaStream_t cs = nullptr;  // communication stream of the bucketed schedule
   std::vector<cudaEvent_t> ev;
+  void* init_mem = nullptr;  // InitTable of the whole-layout work list (lars_init_weights)
+  InitTable init{};
 };
 
 // Tile-aligned buckets of ~equal element counts for every rank (the plan is static: every rank derives
@@ -397,6 +400,41 @@ lars_status_t lars_shard_range(lars_handle_t h, int32_t rank, int64_t* begin, in
 lars_status_t lars_tensor_owner(lars_handle_t h, int32_t* owner) {
   if (!h || !owner) return LARS_ERR_INVALID_ARG;
   std::copy(h->plan.owner.begin(), h->plan.owner.end(), owner);
+  return LARS_OK;
+}
+
+lars_status_t lars_init_weights(lars_handle_t h, float* w, uint64_t seed, void* stream) {
+  if (!h || !w) return LARS_ERR_INVALID_ARG;
+  if (h->device < 0) return LARS_ERR_NO_DEVICE;
+  if (!aligned256(w)) return LARS_ERR_ALIGNMENT;
+  DeviceGuard dg(h->device);
+  if (!h->init_mem) {  // per-layer table of the whole-layout work list, uploaded once
+    const WorkList& wl = h->full.wl;
+    const size_t n = std::max<size_t>(wl.tensors.size(), 1);
+    std::vector<int64_t> off(n, 0);
+    std::vector<int32_t> layer(n, 0), kind(n, 0);
+    std::vector<double> sigma(n, 0.0);
+    for (size_t i = 0; i < wl.tensors.size(); ++i) {
+      const int32_t l = wl.tensors[i];
+      off[i] = h->plan.offset[l];
+      layer[i] = l;
+      kind[i] = h->plan.kind[l];
+      const int64_t fi = h->plan.fan_in[l] > 0 ? h->plan.fan_in[l] : h->plan.numel[l];
+      sigma[i] = std::sqrt(2.0 / (double)fi);
+    }
+    const size_t bytes = n * (8 + 4 + 4 + 8) + 256;
+    if (cudaMalloc(&h->init_mem, bytes) != cudaSuccess) { h->init_mem = nullptr; return LARS_ERR_OOM; }
+    char* p = (char*)h->init_mem;
+    CUDA_OR(cudaMemcpy(p, off.data(), n * 8, cudaMemcpyHostToDevice));
+    CUDA_OR(cudaMemcpy(p + n * 8, sigma.data(), n * 8, cudaMemcpyHostToDevice));
+    CUDA_OR(cudaMemcpy(p + n * 16, layer.data(), n * 4, cudaMemcpyHostToDevice));
+    CUDA_OR(cudaMemcpy(p + n * 20, kind.data(), n * 4, cudaMemcpyHostToDevice));
+    h->init = InitTable{(const int64_t*)p, (const int32_t*)(p + n * 16), (const int32_t*)(p + n * 20),
+                        (const double*)(p + n * 8)};
+  }
+  CUDA_OR(launch_init_weights(h->full.dw, h->init, w, seed, (cudaStream_t)stream));
+  h->full.carry_w = nullptr;  // new weights: any carried norms are stale
+  h->shard.carry_w = nullptr;
   return LARS_OK;
 }
 
@@ -855,6 +893,7 @@ lars_status_t lars_destroy(lars_handle_t h) {
     cudaFree(h->shard.mem);
     cudaFree(h->gred);
     cudaFree(h->gstage);
+    cudaFree(h->init_mem);
     if (h->pinned) cudaFreeHost(h->pinned);
     for (auto& st : h->prof.pending)
       for (auto e : st)

@@ -119,11 +119,14 @@ lars_status_t make_plan(const lars_tensor_t* t, int32_t n, const lars_hparams_t&
   p.P = hp.nranks;
   p.numel.resize(n);
   p.kind.resize(n);
+  p.fan_in.resize(n);
   for (int32_t l = 0; l < n; ++l) {
     if (t[l].numel <= 0 || t[l].numel > ((int64_t)1 << 40)) return LARS_ERR_LAYOUT;
     if (t[l].kind < LARS_KIND_WEIGHT || t[l].kind > LARS_KIND_BN_BETA) return LARS_ERR_LAYOUT;
+    if (t[l].fan_in < 0) return LARS_ERR_LAYOUT;
     p.numel[l] = t[l].numel;
     p.kind[l] = t[l].kind;
+    p.fan_in[l] = t[l].fan_in;
   }
   st = make_schedule(hp, p);
   if (st != LARS_OK) return st;
@@ -133,6 +136,7 @@ lars_status_t make_plan(const lars_tensor_t* t, int32_t n, const lars_hparams_t&
   h = fnv1a(h, &p.P, sizeof p.P);
   h = fnv1a(h, p.numel.data(), p.numel.size() * sizeof(int64_t));
   h = fnv1a(h, p.kind.data(), p.kind.size() * sizeof(int32_t));
+  h = fnv1a(h, p.fan_in.data(), p.fan_in.size() * sizeof(int32_t));
   h = fnv1a(h, p.offset.data(), p.offset.size() * sizeof(int64_t));
   const double hd[] = {hp.base_lr, hp.eta, hp.momentum, hp.weight_decay, hp.eps, hp.warmup_epochs,
                        hp.poly_power, hp.grad_scale};

@@ -37,7 +37,7 @@ class LarsError(RuntimeError):
 
 
 class TensorDesc(ctypes.Structure):
-    _fields_ = [("numel", c_int64), ("kind", c_int32), ("reserved", c_int32)]
+    _fields_ = [("numel", c_int64), ("kind", c_int32), ("fan_in", c_int32)]
 
 
 class HParams(ctypes.Structure):
@@ -70,6 +70,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "lars_shard_range": (c_int32, [h, c_int32, POINTER(c_int64), POINTER(c_int64)]),
         "lars_tensor_owner": (c_int32, [h, POINTER(c_int32)]),
         "lars_layout_hash": (c_int32, [h, POINTER(c_uint64)]),
+        "lars_init_weights": (c_int32, [h, c_void_p, ctypes.c_uint64, c_void_p]),
         "lars_work_info": (c_int32, [h, c_int32, POINTER(c_int32), POINTER(c_int32), POINTER(c_int32)]),
         "lars_step": (c_int32, [h, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
         "lars_step_host_grad": (c_int32, [h, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
@@ -166,11 +167,12 @@ class Lars:
     """A planned LARS step: ``lars_init`` on construction, ``lars_destroy`` on close()."""
 
     def __init__(self, tensors, device: int = 0, **hparams):
-        """tensors: iterable of (numel, kind) with kind a name in KIND or its code.
+        """tensors: iterable of (numel, kind[, fan_in]) with kind a name in KIND or its code.
         hparams: fields of lars_hparams_t (base_lr is required)."""
         lib = load_library()
-        descs = [(int(n), KIND[k] if isinstance(k, str) else int(k)) for n, k in tensors]
-        arr = (TensorDesc * max(1, len(descs)))(*[TensorDesc(n, k, 0) for n, k in descs])
+        descs = [(int(t[0]), KIND[t[1]] if isinstance(t[1], str) else int(t[1]), int(t[2]) if len(t) > 2 else 0)
+                 for t in tensors]
+        arr = (TensorDesc * max(1, len(descs)))(*[TensorDesc(n, k, f) for n, k, f in descs])
         self.hp = default_hparams(**hparams)
         self.n = len(descs)
         self.device = device
@@ -204,6 +206,10 @@ class Lars:
         o = (c_int32 * self.n)()
         _check(self._lib.lars_tensor_owner(self._h, o), "lars_tensor_owner")
         return list(o)
+
+    def init_weights(self, w, seed: int, stream=None) -> None:
+        """Parallel deterministic initialization: same seed -> same weights everywhere."""
+        _check(self._lib.lars_init_weights(self._h, _ptr(w), seed, _stream(stream)), "lars_init_weights")
 
     def work_info(self, rank: int = -1) -> dict:
         t, sg, c = c_int32(), c_int32(), c_int32()

@@ -183,6 +183,16 @@ def main():
             print(json.dumps(report), flush=True)
             dist.destroy_process_group()
             sys.exit(1)
+    # parallel deterministic initialization: every rank initializes its own replica from
+    # the same seed; the replicas are bitwise identical with zero bytes broadcast
+    lay_i = LY.resnet50()
+    hi = PK.Lars([(x.numel, x.kind, x.fan_in) for x in lay_i], device=local, nranks=P, **hp_kwargs())
+    w_i = torch.zeros(hi.padded_numel, dtype=torch.float32, device=dev)  # padding is not written
+    hi.init_weights(w_i, 100000)
+    torch.cuda.synchronize()
+    report["parallel_init_identical"] = all_same(w_i)
+    assert report["parallel_init_identical"]
+    hi.close()
     # layout disagreement across ranks -> LARS_ERR_LAYOUT on every rank
     bad = LY.tiny() if rank == 0 else LY.tiny()[:2]
     h = PK.Lars([(x.numel, x.kind) for x in bad], device=local, nranks=P, **hp_kwargs())

@@ -280,3 +280,44 @@ def test_p14_bf16_widening():
     bits = np.array([0x3F80, 0xBF80, 0x0000, 0x4049, 0x0001, 0x7F7F], np.uint16)
     want = [1.0, -1.0, 0.0, 3.140625, 2.0 ** -133, (2 - 2.0 ** -7) * 2.0 ** 127]
     assert O.to_double(bits).tolist() == want
+
+
+# ---------------------------------------------------------------- parallel initialization (NEXT-f4)
+def test_philox4x64_known_answer():
+    # Random123 known-answer vector (Salmon et al., SC'11): philox4x64-10, counter 0, key 0
+    assert O.philox4x64_10((0, 0, 0, 0), (0, 0)) == (0x16554D9ECA36314C, 0xDB20FE9D672D0FDC,
+                                                     0xD7E772CEE186176B, 0x7E68B68AEC7BA23B)
+
+
+@pytest.mark.parametrize("key,ctr", [((0, 0), (0, 0, 0, 0)), ((100000, 0x4C415253), (7, 3, 0, 0)),
+                                     ((2 ** 64 - 1, 12345), (2 ** 40, 2, 5, 9))])
+def test_philox4x64_matches_numpy_library(key, ctr):
+    # numpy.random.Philox is Philox4x64-10 and advances its counter before the first block
+    bg = np.random.Philox(key=np.array(key, dtype=np.uint64), counter=np.array(ctr, dtype=np.uint64))
+    got = tuple(int(x) for x in bg.random_raw(4))
+    nxt = (ctr[0] + 1,) + tuple(ctr[1:])
+    assert O.philox4x64_10(nxt, key) == got
+
+
+def test_truncated_normal_transform_matches_scipy():
+    from scipy.stats import truncnorm
+
+    u = O.init_uniform(100000, 3, 4096)
+    assert (u >= 0).all() and (u < 1).all()
+    w = O.init_weights(["weight"], [4096], [2], 100000)[0]  # sigma = 1 (fan_in 2)
+    # same u through a library truncated-normal quantile function
+    ref = truncnorm(-2.0, 2.0).ppf(O.init_uniform(100000, 0, 4096))
+    np.testing.assert_allclose(w, ref, rtol=1e-9, atol=1e-12)
+
+
+def test_init_weights_distribution_and_constant_kinds():
+    n = 65536
+    w = O.init_weights(["weight", "bn_gamma", "bn_beta", "bias"], [n, 7, 7, 3], [147, 0, 0, 0], 100000)
+    sigma = math.sqrt(2.0 / 147)
+    z = w[0] / sigma
+    assert np.abs(z).max() <= 2.0 and abs(z.mean()) < 0.02
+    assert abs(z.std() - 0.8796256610342398) < 0.01  # std of N(0,1) truncated at +-2
+    assert (w[1] == 1.0).all() and not w[2].any() and not w[3].any()
+    # a different seed or layer gives different weights; the same seed gives the same
+    assert not np.array_equal(w[0], O.init_weights(["weight"], [n], [147], 100001)[0])
+    assert np.array_equal(w[0], O.init_weights(["weight"], [n], [147], 100000)[0])
