@@ -105,14 +105,28 @@ typedef struct {
                             norms of bucket k-1, and the update of bucket k overlaps the weight
                             broadcast of bucket k-1 ("several megabytes"). 0/1 =
                             one ncclReduceScatter + one ncclAllGather (default)                    */
+  int32_t decay;         /* lars_decay_t after the warm-up (default LARS_DECAY_POLY)              */
+  int32_t n_milestones;  /* LARS_DECAY_STEP: number of milestones (0..8)                          */
   int32_t reserved;      /* must be 0                                                             */
+  double step_gamma;     /* LARS_DECAY_STEP: factor applied at every milestone (default 0.1)       */
+  double milestones[8];  /* LARS_DECAY_STEP: ascending milestones in epochs                        */
 } lars_hparams_t;
+
+/* Learning-rate decay after the warm-up ("step, polynomial, linear"):
+ *   LARS_DECAY_POLY: base * ((T - t) / (T - W))^p   (p = 1 linear, p = 0 constant)
+ *   LARS_DECAY_STEP: base * step_gamma^k, k = number of milestones M_j = round(milestones[j] * ipe) <= t */
+typedef enum { LARS_DECAY_POLY = 0, LARS_DECAY_STEP = 1 } lars_decay_t;
 
 /* Carry the weight norms: K2 also produces sum(w_new^2) for every layer, so the next step's K1 reads only
  * g (8 -> 4 B/param of norm traffic with fp32 g, 6 -> 2 with fp16). Valid as long as the weights are
  * changed by this handle's steps only: passing a different w pointer invalidates automatically; call
  * lars_invalidate_carried_norms after modifying w in place any other way (e.g. loading a checkpoint). */
 #define LARS_FLAG_CARRY_WNORM 1u
+
+/* Momentum form of SPEC.md:186 ("velocity accumulates (grad + wd w) and lr multiplies at application"):
+ * v <- mu v + (s g + beta_l w);  w <- w - lr(t) lambda v.   Default (flag clear) is reading #2:
+ * v <- mu v + lr(t) lambda (s g + beta_l w);  w <- w - v.  Both agree on a step from v = 0. */
+#define LARS_FLAG_LR_AT_APPLY 2u
 
 typedef struct lars_ctx* lars_handle_t;
 

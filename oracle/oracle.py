@@ -52,6 +52,10 @@ class HParams:
     dataset_size: int = 1_280_000
     total_epochs: int = 90         # PAPER.md:211; log epochs 0..89
     grad_scale: float = 1.0
+    decay: str = "poly"            # "poly" or "step" ("step, polynomial, linear")
+    step_gamma: float = 0.1        # step decay factor per milestone
+    milestones: tuple = ()         # step decay milestones in epochs
+    momentum_form: str = "velocity"  # reading #2 ("velocity") or SPEC.md:186's lr-at-apply ("apply")
 
 
 # ----------------------------------------------------------------------------------------------
@@ -78,11 +82,17 @@ def lr_at(hp: HParams, t: int) -> float:
     evaluated as base * ((T-t)/(T-W))^p — the same number, written without the cancellation of
     1 - (t-W)/(T-W) near t = T-1 (one rounding in the ratio instead of two).
     """
-    _, T, W = schedule(hp)
+    ipe, T, W = schedule(hp)
     if not (0 <= t < T):
         raise ValueError(f"iteration {t} outside [0, {T})")
     if t < W:
         return hp.base_lr * (t + 1) / W
+    if hp.decay == "step":  # base * gamma^(number of milestones reached); milestones in epochs -> iterations
+        lr = hp.base_lr
+        for m in hp.milestones:
+            if t >= int(math.floor(m * ipe + 0.5)):
+                lr *= hp.step_gamma
+        return lr
     return hp.base_lr * ((T - t) / (T - W)) ** hp.poly_power
 
 
@@ -174,7 +184,7 @@ def step(kinds: list, hp: HParams, t: int, w: list, g_ranks: list, m: list) -> S
 
     w_new, m_new, m_env, w_env = [], [], [], []
     for l in range(L):
-        a, b, c, d = update(hp, lr, lam[l], beta[l], W64[l], G[l], M64[l], absg[l])
+        a, b, c, d = update(hp, lr, lam[l], beta[l], W64[l], G[l], M64[l], absg[l], hp.momentum_form)
         w_new.append(a)
         m_new.append(b)
         m_env.append(c)
@@ -182,14 +192,19 @@ def step(kinds: list, hp: HParams, t: int, w: list, g_ranks: list, m: list) -> S
     return StepResult(w_new, m_new, w_norm, g_norm, list(lam), lr, False, m_env, w_env)
 
 
-def update(hp: HParams, lr: float, lam: float, beta: float, w, G, m, abs_g_sum):
-    """O6 for one layer (or any subset of its elements) given its trust ratio lambda and decay beta_l:
-    u = G + beta*w; v = mu*m + lr*lambda*u; w_new = w - v (reading #2). G is the combined, scaled gradient
-    and abs_g_sum = |s| sum_r |g_r| (for the magnitude envelopes of reading #17).
-    Returns (w_new, v, E_m, E_w) in float64."""
+def update(hp: HParams, lr: float, lam: float, beta: float, w, G, m, abs_g_sum, form: str = "velocity"):
+    """O6 for one layer (or any subset of its elements) given its trust ratio lambda and decay beta_l.
+    form "velocity" (reading #2): u = G + beta*w; v = mu*m + lr*lambda*u; w_new = w - v.
+    form "apply" (SPEC.md:186):   u = G + beta*w; v = mu*m + u;           w_new = w - lr*lambda*v.
+    G is the combined, scaled gradient and abs_g_sum = |s| sum_r |g_r| (for the magnitude envelopes of
+    reading #17). Returns (w_new, v, E_m, E_w) in float64."""
     w = np.asarray(w, dtype=np.float64)
     m = np.asarray(m, dtype=np.float64)
     u = G + beta * w                                   # g + beta*w
+    if form == "apply":
+        v = hp.momentum * m + u                        # v <- mu*v + (g + beta*w)
+        e_m = abs(hp.momentum) * np.abs(m) + abs_g_sum + abs(beta) * np.abs(w)
+        return w - lr * lam * v, v, e_m, np.abs(w) + abs(lr * lam) * e_m
     v = hp.momentum * m + lr * lam * u                 # v <- mu*v + lr*lambda*(g + beta*w)
     e_m = abs(hp.momentum) * np.abs(m) + abs(lr * lam) * (abs_g_sum + abs(beta) * np.abs(w))
     # w - v is computed from |w| and every term of v: its envelope is |w| + E_m (reading #17)

@@ -144,6 +144,7 @@ struct Hyper {
   double eta, weight_decay, eps, grad_scale;
   float mu, grad_scale_f;
   bool carry;                // LARS_FLAG_CARRY_WNORM
+  bool lr_at_apply;          // LARS_FLAG_LR_AT_APPLY (SPEC.md:186 momentum form)
 };
 
 // g_shift: the gradient of flat element e is g[e - g_shift] (the DP step reads its reduced shard).

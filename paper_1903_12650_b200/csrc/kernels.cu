@@ -501,13 +501,23 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_norms_kernel(DevWor
 }
 
 // ---------------------------------------------------------------- K2: fused update
-__device__ __forceinline__ void upd8(F8& w, F8& m, const F8& g, float s, float c, float b, float mu) {
+__device__ __forceinline__ void upd8(F8& w, F8& m, const F8& g, float s, float c, float b, float mu, bool apply) {
+  if (!apply) {  // reading #2: lr*lambda inside the velocity
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const float u = fmaf(b, w.v[i], s * g.v[i]);  // s*g + beta_l*w
-    const float v = fmaf(mu, m.v[i], c * u);       // mu*v + lr*lambda*(...)
-    w.v[i] = w.v[i] - v;
-    m.v[i] = v;
+    for (int i = 0; i < 8; ++i) {
+      const float u = fmaf(b, w.v[i], s * g.v[i]);  // s*g + beta_l*w
+      const float v = fmaf(mu, m.v[i], c * u);       // mu*v + lr*lambda*(...)
+      w.v[i] = w.v[i] - v;
+      m.v[i] = v;
+    }
+  } else {       // velocity of (s*g + beta_l*w), lr*lambda at the weight step
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float u = fmaf(b, w.v[i], s * g.v[i]);
+      const float v = fmaf(mu, m.v[i], u);
+      w.v[i] = fmaf(-c, v, w.v[i]);
+      m.v[i] = v;
+    }
   }
 }
 
@@ -577,11 +587,12 @@ __device__ __forceinline__ void update_item(int32_t item, const DevWork& wk, con
     for (int32_t i = (ng << 3) + lane; i < ck.len; i += 32) {  // ragged tensor tail (< 8 elements)
       const float wv = wp[i], mv = mp[i];
       const float u = fmaf(b, wv, s * Grad<DT>::load1(g, gi + i));
-      const float v = fmaf(mu, mv, cf * u);
-      wp[i] = wv - v;
+      const float v = hy.lr_at_apply ? fmaf(mu, mv, u) : fmaf(mu, mv, cf * u);
+      const float wn = hy.lr_at_apply ? fmaf(-cf, v, wv) : wv - v;
+      wp[i] = wn;
       mp[i] = v;
-      ws.store1(ck.begin + i, wv - v);
-      if (CARRY) aw = fma((double)(wv - v), (double)(wv - v), aw);
+      ws.store1(ck.begin + i, wn);
+      if (CARRY) aw = fma((double)wn, (double)wn, aw);
     }
     int32_t j = ng - 1 - lane;
     for (; j - 32 >= 0; j -= 64) {
@@ -589,8 +600,8 @@ __device__ __forceinline__ void update_item(int32_t item, const DevWork& wk, con
       F8 w0 = ld8_rw(wp + 8 * j), w1 = ld8_rw(wp + 8 * j1);
       const F8 g0 = Grad<DT>::load8(g, gi + 8 * j), g1 = Grad<DT>::load8(g, gi + 8 * j1);
       F8 m0 = ld8_rw(mp + 8 * j), m1 = ld8_rw(mp + 8 * j1);
-      upd8(w0, m0, g0, s, cf, b, mu);
-      upd8(w1, m1, g1, s, cf, b, mu);
+      upd8(w0, m0, g0, s, cf, b, mu, hy.lr_at_apply);
+      upd8(w1, m1, g1, s, cf, b, mu, hy.lr_at_apply);
       st8(wp + 8 * j, w0);
       st8(mp + 8 * j, m0);
       st8(wp + 8 * j1, w1);
@@ -605,7 +616,7 @@ __device__ __forceinline__ void update_item(int32_t item, const DevWork& wk, con
     if (j >= 0) {
       F8 w0 = ld8_rw(wp + 8 * j), m0 = ld8_rw(mp + 8 * j);
       const F8 g0 = Grad<DT>::load8(g, gi + 8 * j);
-      upd8(w0, m0, g0, s, cf, b, mu);
+      upd8(w0, m0, g0, s, cf, b, mu, hy.lr_at_apply);
       st8(wp + 8 * j, w0);
       st8(mp + 8 * j, m0);
       ws.store8(ck.begin + 8 * j, w0);

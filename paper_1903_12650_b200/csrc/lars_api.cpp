@@ -316,6 +316,7 @@ void lars_hparams_default(lars_hparams_t* hp) {
   hp->grad_dtype = LARS_F16;
   hp->nranks = 1;
   hp->tile_elems = 0;
+  hp->step_gamma = 0.1;
 }
 
 const char* lars_version(void) { return "lars-b200 0.1 (sm_100a)"; }
@@ -473,7 +474,8 @@ static lars_status_t check_step_args(lars_handle_t h, const void* w, const void*
 
 static Hyper hyper(lars_handle_t h, int64_t iter, int64_t* iter_dev = nullptr) {
   return Hyper{h->lr_d, iter, iter_dev, h->plan.T, h->hp.eta, h->hp.weight_decay, h->hp.eps, h->hp.grad_scale,
-               (float)h->hp.momentum, (float)h->hp.grad_scale, (h->hp.flags & LARS_FLAG_CARRY_WNORM) != 0};
+               (float)h->hp.momentum, (float)h->hp.grad_scale, (h->hp.flags & LARS_FLAG_CARRY_WNORM) != 0,
+               (h->hp.flags & LARS_FLAG_LR_AT_APPLY) != 0};
 }
 
 // Carry mode: the norms K2 left are only valid for the weights it wrote. A different weight buffer (or

@@ -30,6 +30,15 @@ lars_status_t validate_hparams(const lars_hparams_t& hp) {
   if (hp.nranks < 1 || hp.nranks > 4096) return LARS_ERR_INVALID_ARG;
   if (hp.tile_elems < 0) return LARS_ERR_INVALID_ARG;
   if (hp.buckets < 0 || hp.buckets > 1024 || hp.reserved != 0) return LARS_ERR_INVALID_ARG;
+  if (hp.decay != LARS_DECAY_POLY && hp.decay != LARS_DECAY_STEP) return LARS_ERR_INVALID_ARG;
+  if (hp.flags & ~(LARS_FLAG_CARRY_WNORM | LARS_FLAG_LR_AT_APPLY)) return LARS_ERR_INVALID_ARG;
+  if (hp.decay == LARS_DECAY_STEP) {
+    if (hp.n_milestones < 0 || hp.n_milestones > 8 || !fin(hp.step_gamma) || hp.step_gamma < 0)
+      return LARS_ERR_INVALID_ARG;
+    for (int i = 0; i < hp.n_milestones; ++i)
+      if (!fin(hp.milestones[i]) || hp.milestones[i] < 0 || (i && hp.milestones[i] < hp.milestones[i - 1]))
+        return LARS_ERR_INVALID_ARG;
+  }
   return LARS_OK;
 }
 
@@ -45,11 +54,20 @@ static lars_status_t make_schedule(const lars_hparams_t& hp, Plan& p) {
   p.W = (int64_t)std::floor(hp.warmup_epochs * (double)p.ipe + 0.5);
   if (p.W > p.T || p.T > (int64_t)1 << 26) return LARS_ERR_INVALID_ARG;
   p.lr.resize(p.T);
+  std::vector<int64_t> M;  // step-decay milestones in iterations (round half up, like W)
+  if (hp.decay == LARS_DECAY_STEP)
+    for (int i = 0; i < hp.n_milestones; ++i) M.push_back((int64_t)std::floor(hp.milestones[i] * (double)p.ipe + 0.5));
   for (int64_t t = 0; t < p.T; ++t) {
-    if (t < p.W)
+    if (t < p.W) {
       p.lr[t] = hp.base_lr * (double)(t + 1) / (double)p.W;
-    else
+    } else if (hp.decay == LARS_DECAY_STEP) {
+      double lr = hp.base_lr;
+      for (int64_t m : M)
+        if (t >= m) lr *= hp.step_gamma;
+      p.lr[t] = lr;
+    } else {
       p.lr[t] = hp.base_lr * std::pow((double)(p.T - t) / (double)(p.T - p.W), hp.poly_power);
+    }
   }
   return LARS_OK;
 }
@@ -139,10 +157,11 @@ lars_status_t make_plan(const lars_tensor_t* t, int32_t n, const lars_hparams_t&
   h = fnv1a(h, p.fan_in.data(), p.fan_in.size() * sizeof(int32_t));
   h = fnv1a(h, p.offset.data(), p.offset.size() * sizeof(int64_t));
   const double hd[] = {hp.base_lr, hp.eta, hp.momentum, hp.weight_decay, hp.eps, hp.warmup_epochs,
-                       hp.poly_power, hp.grad_scale};
+                       hp.poly_power, hp.grad_scale, hp.step_gamma, (double)hp.decay, (double)hp.flags};
   h = fnv1a(h, hd, sizeof hd);
   const int64_t hi[] = {hp.global_batch, hp.dataset_size, hp.total_epochs, hp.grad_dtype, hp.shard_policy};
   h = fnv1a(h, hi, sizeof hi);
+  h = fnv1a(h, p.lr.data(), p.lr.size() * sizeof(double));  // the whole schedule, milestones included
   p.hash = h;
   return LARS_OK;
 }

@@ -23,7 +23,9 @@ KIND = {"weight": 0, "bias": 1, "bn_gamma": 2, "bn_beta": 3}
 DTYPE = {"f32": 0, "f16": 1, "bf16": 2}
 DTYPE_BYTES = {"f32": 4, "f16": 2, "bf16": 2}
 SHARD_POLICY = {"contiguous": 0, "lpt": 1}
+DECAY = {"poly": 0, "step": 1}
 FLAG_CARRY_WNORM = 1
+FLAG_LR_AT_APPLY = 2
 
 
 class LarsLibraryMissing(RuntimeError):
@@ -46,7 +48,8 @@ class HParams(ctypes.Structure):
                 ("grad_scale", c_double), ("global_batch", c_int64), ("dataset_size", c_int64),
                 ("total_epochs", c_int32), ("grad_dtype", c_int32), ("nranks", c_int32),
                 ("tile_elems", c_int32), ("shard_policy", c_int32), ("flags", ctypes.c_uint32),
-                ("buckets", c_int32), ("reserved", c_int32)]
+                ("buckets", c_int32), ("decay", c_int32), ("n_milestones", c_int32), ("reserved", c_int32),
+                ("step_gamma", c_double), ("milestones", c_double * 8)]
 
 
 _lib = None
@@ -146,7 +149,18 @@ def default_hparams(**kw) -> HParams:
             v = DTYPE[v]
         if k == "shard_policy" and isinstance(v, str):
             v = SHARD_POLICY[v]
+        if k == "decay" and isinstance(v, str):
+            v = DECAY[v]
+        if k == "milestones":
+            hp.n_milestones = len(v)
+            for i, x in enumerate(v):
+                hp.milestones[i] = float(x)
+            continue
+        if k == "momentum_form":
+            continue
         setattr(hp, k, v)
+    if "momentum_form" in kw:  # oracle-style spelling of LARS_FLAG_LR_AT_APPLY
+        hp.flags = (hp.flags & ~FLAG_LR_AT_APPLY) | (FLAG_LR_AT_APPLY if kw["momentum_form"] == "apply" else 0)
     return hp
 
 

@@ -164,6 +164,8 @@ def main():
              ("fused-tiny-int", LY.tiny(), "f16", 80, dict(kind="integer", fused=True)),
              ("fused-r50-f16", lay_r50, "f16", 719, dict(fused=True)),
              ("fused-r50-f16-carry", lay_r50, "f16", 720, dict(fused=True, flags=1)),
+             ("fused-r50-f16-apply-step", lay_r50, "f16", 481, dict(fused=True, flags=1, momentum_form="apply",
+                                                                   decay="step", milestones=(30, 60))),
              ("fused-random-bf16", LY.random_layout(np.random.default_rng(8), 29), "bf16", 700, dict(fused=True)),
              ("fused-zipf-f32", LY.skew1b("zipf", n_tensors=200, total=4_000_000), "f32", 500, dict(fused=True)),
              ("fused-nan-in-split-layer", LY.skew1b("zipf", n_tensors=50, total=1_000_000), "f16", 100,

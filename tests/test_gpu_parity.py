@@ -264,3 +264,22 @@ def test_carried_norms_invalidation():
     pre_w, pre_m = s.state()
     s.step(103)
     s.check(103, pre_w, [g], pre_m, TOL_F32, tag="new w buffer")
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f16"])
+@pytest.mark.parametrize("form", ["velocity", "apply"])
+def test_variants_step_decay_and_momentum_form(dtype, form):
+    """NEXT-f3 variants: step decay across a milestone and SPEC.md:186's lr-at-apply
+    momentum form, chained over 5 steps with carried norms; each step against the oracle."""
+    _torch()
+    lay = LY.tiny() + LY.random_layout(np.random.default_rng(41), 12)
+    s = GpuStep(lay, grad_dtype=dtype, decay="step", milestones=(30, 60), step_gamma=0.1, momentum_form=form,
+                flags=1)
+    s.upload(G.weights(lay), G.grads(lay, 0, 0, dtype), G.momentum(lay, 1e-3))
+    for t in range(478, 483):  # epoch-30 milestone at t = 480
+        g = G.grads(lay, 0, t, dtype)
+        s.g = to_dev(G.pack(g, s.h.offsets, s.h.padded_numel))
+        pre_w, pre_m = s.state()
+        s.step(t)
+        r, _ = s.check(t, pre_w, [g], pre_m, TOL_F32, tag=f"{form} {dtype} t={t}")
+        assert r.lr == s.h.lr_at(t) and r.lr == (32.0 if t < 480 else 32.0 * 0.1)

@@ -71,7 +71,9 @@ def test_lpt_is_deterministic_and_hash_identifies_plan():
 
 def test_schedule_matches_oracle_for_every_iteration():
     for kw in (dict(base_lr=32.0), dict(base_lr=8.0, poly_power=1.0), dict(base_lr=3.0, warmup_epochs=2.5),
-               dict(base_lr=1.0, global_batch=32768, poly_power=0.0), dict(base_lr=0.5, warmup_epochs=0.0)):
+               dict(base_lr=1.0, global_batch=32768, poly_power=0.0), dict(base_lr=0.5, warmup_epochs=0.0),
+               dict(base_lr=8.0, decay="step", milestones=(30, 60, 80), step_gamma=0.1),
+               dict(base_lr=2.0, decay="step", milestones=(0.5, 45.3), step_gamma=0.5, warmup_epochs=0.0)):
         h = P.Lars([(10, "weight")], device=-1, **kw)
         hp = O.HParams(**{k: v for k, v in kw.items()})
         ipe, T, W = O.schedule(hp)

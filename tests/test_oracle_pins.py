@@ -321,3 +321,30 @@ def test_init_weights_distribution_and_constant_kinds():
     # a different seed or layer gives different weights; the same seed gives the same
     assert not np.array_equal(w[0], O.init_weights(["weight"], [n], [147], 100001)[0])
     assert np.array_equal(w[0], O.init_weights(["weight"], [n], [147], 100000)[0])
+
+
+# ---------------------------------------------------------------- optimizer variants (NEXT-f3)
+def test_step_decay_hand_values():
+    # PAPER.md:102 "step" decay: base 8, warm-up 1 epoch (W = 16), milestones 30/60/80 epochs, gamma 0.1
+    h = hp(base_lr=8.0, warmup_epochs=1.0, decay="step", milestones=(30, 60, 80), step_gamma=0.1)
+    want = {15: 8.0, 16: 8.0, 479: 8.0, 480: 0.8, 959: 0.8, 960: 0.08, 1279: 0.08, 1280: 0.008, 1439: 0.008}
+    for t, v in want.items():
+        assert O.lr_at(h, t) == pytest.approx(v, rel=1e-15), t
+    assert O.lr_at(h, 3) == 2.0  # the warm-up is unchanged
+
+
+def test_momentum_form_lr_at_apply():
+    # SPEC.md:186 form: v <- mu v + (g + beta w); w <- w - lr lambda v. Warm-up lr(0) = 0.4, lr(1) = 0.8:
+    # v1 = g, w1 = w0 - 0.4 g; v2 = 1.9 g, w2 = w1 - 0.8 * 1.9 g = w0 - 1.92 g (reading #2 gives 1.56 g)
+    g = np.array([0.5], np.float32)
+    h = hp(momentum_form="apply")
+    r1 = O.step(["bias"], h, 0, [np.array([1.0], np.float32)], [[g]], [np.zeros(1, np.float32)])
+    r2 = O.step(["bias"], h, 1, r1.w, [[g]], r1.m)
+    assert float(r2.m[0][0]) == pytest.approx(1.9 * 0.5, rel=1e-15)
+    assert float(r2.w[0][0]) == pytest.approx(1.0 - 1.92 * 0.5, rel=1e-15)
+    # both forms agree on the first step from v = 0
+    ra = O.step(["weight"], hp(), 5, [np.full(8, 0.3, np.float32)], [[np.full(8, 0.01, np.float32)]],
+                [np.zeros(8, np.float32)])
+    rb = O.step(["weight"], h, 5, [np.full(8, 0.3, np.float32)], [[np.full(8, 0.01, np.float32)]],
+                [np.zeros(8, np.float32)])
+    np.testing.assert_allclose(ra.w[0], rb.w[0], rtol=1e-15)
