@@ -22,9 +22,16 @@ constexpr int kThreads = 256;           // threads per CTA of K1 / K2
 #ifndef LARS_NORM_UNROLL
 #define LARS_NORM_UNROLL 2
 #endif
+#ifndef LARS_NORM_UNROLL_G
+#define LARS_NORM_UNROLL_G 4
+#endif
 constexpr int kCtasPerSm = LARS_NORM_CTAS_PER_SM;      // K1 resident CTAs per SM (one static tile each)
 // fused F1 CTAs per SM: 2 ranks fit 64 registers (4 CTAs/SM); 3-8 ranks' loads per vector need 128 (2/SM)
 constexpr int dp_norm_ctas_per_sm(int nranks) { return nranks <= 2 ? 4 : 2; }
+#ifndef LARS_DP_TILES_PER_CTA
+#define LARS_DP_TILES_PER_CTA 1
+#endif
+constexpr int kDpTilesPerCta = LARS_DP_TILES_PER_CTA;  // fused F1/F2: tiles per CTA
 #ifndef LARS_NORM_TILES_PER_CTA
 #define LARS_NORM_TILES_PER_CTA 1
 #endif
@@ -161,6 +168,8 @@ struct DpFused {
   float* gred;                    // fp32 reduced shard (S elements)
   unsigned long long* epoch;      // local step counter (advanced by F1's final CTA)
   int64_t* step_iter;             // the iteration of the current step, recorded by F1
+  unsigned long long* go;         // F1 entry: CTA 0's "all ranks are in" flag (= epoch + 1)
+  unsigned* done;                 // F2 exit: CTAs counted out (the last one syncs with the other ranks)
   bool mcast;                     // NVLS multicast all-gather (multimem.st) instead of per-peer stores
 };
 // F1 (reduce + norms, grid_norm CTAs), FX (exchange + finish), F2 (update + gather, grid_update CTAs);

@@ -154,12 +154,15 @@ __device__ __forceinline__ unsigned smid() {
     unsigned long long* _p = g_trace + ((size_t)(k) * 4096 + blockIdx.x) * 4; \
     _p[0] = _t0; _p[1] = gtimer(); _p[2] = smid(); _p[3] = gridDim.x;         \
   }
+#define TRACE_MARK(k)                                                         \
+  if (threadIdx.x == 0 && g_trace) g_trace[((size_t)(k) * 4096 + blockIdx.x) * 4 + 2] = gtimer();
 extern "C" int lars_trace_arm(void* buf) {
   return (int)cudaMemcpyToSymbol(g_trace, &buf, sizeof buf);
 }
 #else
 #define TRACE_BEGIN
 #define TRACE_END(k)
+#define TRACE_MARK(k)
 #endif
 
 // ---------------------------------------------------------------- gradient sources for K1
@@ -167,7 +170,7 @@ extern "C" int lars_trace_arm(void* buf) {
 template <int DT>
 struct LocalGrad {
   static constexpr int kUnroll = kNormUnroll;  // (w, g) groups per lane per iteration
-  static constexpr int kUnrollG = 4;           // g-only groups per lane per iteration (carried norms)
+  static constexpr int kUnrollG = LARS_NORM_UNROLL_G;  // g-only groups per lane per iteration (carried norms)
   const void* g;
   int64_t shift;
   __device__ __forceinline__ F8 load8(int64_t e) const { return Grad<DT>::load8_keep(g, e - shift); }
@@ -274,8 +277,12 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
   // Phase A: the warps of the CTA stream the tile's chunks independently (no block barrier per layer);
   // chunk partials stay in shared memory.
   const int32_t c0 = wk.tile_chunk[tile], c1 = wk.tile_chunk[tile + 1];
+  // chunk descriptors are prefetched one iteration ahead (their load would otherwise add a round trip
+  // in front of every chunk's data loads)
+  Seg nxt = (c0 + warp < c1) ? wk.chunks[c0 + warp] : Seg{0, 0, 0};
   for (int32_t c = c0 + warp; c < c1; c += kWarps) {
-    const Seg ck = wk.chunks[c];
+    const Seg ck = nxt;
+    if (c + kWarps < c1) nxt = wk.chunks[c + kWarps];
     const float* wp = w + ck.begin;
     const int64_t gi = ck.begin;  // element index handed to the gradient source
     const int32_t ng = ck.len >> 3;
@@ -428,7 +435,7 @@ __device__ __forceinline__ int32_t take_ticket(unsigned long long* t, int32_t ni
 // dynamic (kNormDynamic).
 // Returns true on thread 0 of the CTA that completed the step's layer count (data-parallel mode: the
 // caller then publishes this rank's C3 shares).
-template <bool CARRY, class GL>
+template <bool CARRY, class GL, bool DYN = kNormDynamic>
 __device__ __forceinline__ bool norms_body(const DevWork& wk, const DevScratch& sc, const Hyper& hy,
                                            const float* __restrict__ w, const GL& gl) {
   __shared__ double sm_cw[kMaxTileChunks], sm_cg[kMaxTileChunks];
@@ -440,7 +447,7 @@ __device__ __forceinline__ bool norms_body(const DevWork& wk, const DevScratch& 
   __syncthreads();
   // carry mode: the previous K2 left sum(w_new^2) per chunk; valid until the host invalidates it
   const bool carried = CARRY && *(volatile const int32_t*)sc.wnext_valid != 0;
-  if (kNormDynamic) {  // tiles handed out by a ticket counter (faster CTAs take more tiles)
+  if (DYN) {  // tiles handed out by a ticket counter (faster CTAs take more tiles)
     __shared__ int32_t s_tile;
     if (threadIdx.x == 0) s_tile = take_ticket(sc.ticket + 0, wk.ntiles, gridDim.x);
     __syncthreads();
@@ -765,18 +772,40 @@ template <int DT, bool CARRY, int NP>
 __global__ void __launch_bounds__(kThreads, dp_norm_ctas_per_sm(NP)) lars_dp_reduce_norms_kernel(DevWork wk, DevScratch sc,
                                                                                     Hyper hy, const float* w,
                                                                                     DpFused f) {
-  {  // CTA b of every rank is running => every rank's gradient for this step is complete
-    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), f.dc, ncclTeamTagLsa(), blockIdx.x);
-    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+  TRACE_BEGIN
+  // Entry: every rank's gradient for this step is complete once every rank's F1 is running. CTA 0 alone
+  // syncs with the other ranks (one LSA barrier instead of one per CTA); the others wait for its go flag.
+  // The step epoch cannot move during the entry: the CTA that advances it is the last to finish a tile.
+  {
+    const unsigned long long E = *(volatile const unsigned long long*)f.epoch;
+    if (blockIdx.x == 0) {
+      ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), f.dc, ncclTeamTagLsa(), 0);
+      bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+      if (threadIdx.x == 0) {
+        cuda::atomic_ref<unsigned long long, cuda::thread_scope_system> go(*f.go);
+        go.store(E + 1, cuda::memory_order_release);
+      }
+    } else {
+      if (threadIdx.x == 0) {
+        cuda::atomic_ref<unsigned long long, cuda::thread_scope_system> go(*f.go);
+        while (go.load(cuda::memory_order_acquire) < E + 1) __nanosleep(32);
+      }
+    }
+    __syncthreads();
   }
+  TRACE_MARK(5)
   PeerSumGrad<DT, NP> gl;
 #pragma unroll
   for (int p = 0; p < NP; ++p) gl.gp[p] = p < f.nranks ? ncclGetLsaPointer(f.gwin, 0, p) : nullptr;
   gl.nranks = f.nranks;
   gl.gred = f.gred;
   gl.begin = f.begin;
-  const bool final_cta = norms_body<CARRY>(wk, sc, hy, w, gl);
+  // static tiles (one per CTA): measured faster than 4x finer dynamically scheduled tiles, whose per-tile
+  // overhead outweighs the shorter tail (tools/trace_dp.py)
+  const bool final_cta = norms_body<CARRY, PeerSumGrad<DT, NP>, false>(wk, sc, hy, w, gl);
   if (final_cta || (wk.ntensors == 0 && blockIdx.x == 0 && threadIdx.x == 0)) dp_publish_shares(wk, sc, hy, f);
+  __syncthreads();
+  TRACE_END(2)
 }
 
 template <bool CARRY, bool MCAST>
@@ -784,6 +813,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_dp_update_gather_ke
                                                                                      Hyper hy, float* w, float* m,
                                                                                      DpFused f) {
   __shared__ int32_t s_status;
+  TRACE_BEGIN
   if (threadIdx.x < 32) {
     const int32_t st = dp_collect_shares(wk, sc, hy, f);
     if (threadIdx.x == 0) {
@@ -793,7 +823,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_dp_update_gather_ke
   }
   __syncthreads();
   const bool skip = s_status != 0;
-  if (!skip) {  // items ordered last-part-of-every-tile first (see update_item), striped over this grid
+  // items ordered last-part-of-every-tile first (see update_item), striped statically over this grid
+  if (!skip) {
     if (MCAST) {
       const McastWeights ws{(float*)ncclGetLsaMultimemPointer(f.wwin, 0, f.dc)};
       for (int32_t item = blockIdx.x; item < wk.ntiles * kUpdateSplit; item += gridDim.x)
@@ -809,8 +840,19 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_dp_update_gather_ke
   }
   if (MCAST) asm volatile("fence.acq_rel.sys;" ::: "memory");  // multicast stores before the barrier release
   if (CARRY && !skip && blockIdx.x == 0 && threadIdx.x == 0) *(volatile int32_t*)sc.wnext_valid = 1;
-  {  // CTA b of every rank has stored its weights => after this grid, every rank's w is complete
-    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), f.dc, ncclTeamTagLsa(), blockIdx.x);
+  __syncthreads();
+  TRACE_END(3)
+  // Exit: after this grid every rank's w must be complete. Each CTA makes its peer stores visible and
+  // counts itself out; the last CTA of the grid syncs with the other ranks' last CTAs (one LSA barrier).
+  __shared__ int s_last;
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    s_last = atomicAdd(f.done, 1u) == gridDim.x - 1;
+    if (s_last) *(volatile unsigned*)f.done = 0u;
+  }
+  __syncthreads();
+  if (s_last) {
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), f.dc, ncclTeamTagLsa(), 0);
     bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
   }
 }

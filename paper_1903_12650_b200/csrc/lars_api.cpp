@@ -272,7 +272,7 @@ static lars_status_t setup_fused(lars_ctx* h) {
   f.grid_update = h->sms * kCtasPerSm;
   ncclDevCommRequirements reqs;
   std::memset(&reqs, 0, sizeof reqs);
-  reqs.lsaBarrierCount = std::max(f.grid_norm, f.grid_update) + 1;
+  reqs.lsaBarrierCount = 1;  // one barrier: F1's entry and F2's exit, each taken by a single CTA
   // NVLS multicast all-gather (multimem.st) is opt-in: measured 2x slower than per-peer stores for fp32
   // weights on B200 (profiles/README.md), so per-peer NVLink stores are the default.
   const char* mc_env = getenv("LARS_DP_MCAST");
@@ -571,7 +571,8 @@ lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, cons
   if (r[0] != h->plan.hash || r[1] != h->plan.hash) return LARS_ERR_LAYOUT;
   const int32_t min_tile = h->hp.tile_elems > 0 ? h->hp.tile_elems : kDefaultMinTile;
   const bool fused = fused_eligible(h);
-  const int32_t ntiles_target = h->sms * (fused ? dp_norm_ctas_per_sm(nranks) : kCtasPerSm) * kTilesPerCta;
+  const int32_t ntiles_target =
+      fused ? h->sms * dp_norm_ctas_per_sm(nranks) * kDpTilesPerCta : h->sms * kCtasPerSm * kTilesPerCta;
   h->shard.wl = make_worklist(h->plan, rank, ntiles_target, min_tile);
   h->K = std::max(1, h->hp.buckets);
   if (h->K > 1) {
@@ -668,7 +669,9 @@ static lars_status_t dp_impl(lars_handle_t h, float* w, const void* g, float* m,
   if (h->fused.ok && (void*)w == h->fused.w && g == h->fused.g) {  // fused NVLink path (F1, FX, F2)
     DpFused f{h->fused.dc,   h->fused.gwin, h->fused.wwin,  h->fused.xwin,
               h->rank,       h->plan.P,     begin,          h->fused.gred32,
-              (unsigned long long*)h->fused.state, (int64_t*)((char*)h->fused.state + 8), h->fused.mcast};
+              (unsigned long long*)h->fused.state, (int64_t*)((char*)h->fused.state + 8),
+              (unsigned long long*)((char*)h->fused.state + 16), (unsigned*)((char*)h->fused.state + 24),
+              h->fused.mcast};
     prof_rec(pe, 0, s);
     prof_rec(pe, 1, s);
     CUDA_OR(launch_dp_fused(dt, h->shard.dw, h->shard.sc, hy, w, m, f, h->fused.grid_norm, h->fused.grid_update, s,
