@@ -156,6 +156,8 @@ __device__ __forceinline__ unsigned smid() {
   }
 #define TRACE_MARK(k)                                                         \
   if (threadIdx.x == 0 && g_trace) g_trace[((size_t)(k) * 4096 + blockIdx.x) * 4 + 2] = gtimer();
+#define TRACE_MARK_AT(k, c) \
+  if (threadIdx.x == 0 && g_trace) g_trace[((size_t)(k) * 4096 + blockIdx.x) * 4 + (c)] = gtimer();
 extern "C" int lars_trace_arm(void* buf) {
   return (int)cudaMemcpyToSymbol(g_trace, &buf, sizeof buf);
 }
@@ -163,6 +165,7 @@ extern "C" int lars_trace_arm(void* buf) {
 #define TRACE_BEGIN
 #define TRACE_END(k)
 #define TRACE_MARK(k)
+#define TRACE_MARK_AT(k, c)
 #endif
 
 // ---------------------------------------------------------------- gradient sources for K1
@@ -221,6 +224,23 @@ struct PeerSumGrad {
 
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Launch with programmatic dependent launch: the kernel may become resident while its predecessor
+// drains and must call pdl_wait() before touching anything the predecessor writes.
+template <typename K, typename... Args>
+static cudaError_t launch_pdl(K kernel, int grid, cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
 
 __device__ __forceinline__ void acc8(double& a, const F8& x) {
 #pragma unroll
@@ -721,12 +741,15 @@ __device__ void dp_publish_shares(const DevWork& wk, const DevScratch& sc, const
   const int64_t t = hy.iter_dev ? *(volatile int64_t*)hy.iter_dev : hy.iter;
   *f.step_iter = t;
   if (hy.iter_dev) *(volatile int64_t*)hy.iter_dev = t + 1;
-  for (int p = 0; p < f.nranks; ++p) {
+  for (int p = 0; p < f.nranks; ++p) {  // payloads to every rank first, then one fence, then the flags
     double* slot = (double*)ncclGetLsaPointer(f.xwin, (size_t)f.rank * (n + 1) * sizeof(double), p);
     for (int32_t i = 0; i < n; ++i) slot[1 + i] = sc.c3[i];
-    __threadfence_system();
+  }
+  cuda::atomic_thread_fence(cuda::memory_order_release, cuda::thread_scope_system);
+  for (int p = 0; p < f.nranks; ++p) {
+    double* slot = (double*)ncclGetLsaPointer(f.xwin, (size_t)f.rank * (n + 1) * sizeof(double), p);
     cuda::atomic_ref<unsigned long long, cuda::thread_scope_system> flag(*(unsigned long long*)slot);
-    flag.store(epoch, cuda::memory_order_release);
+    flag.store(epoch, cuda::memory_order_relaxed);
   }
   for (int32_t i = 0; i < n; ++i) sc.c3[i] = 0.0;  // next step's shares start from zero
 }
@@ -773,6 +796,8 @@ __global__ void __launch_bounds__(kThreads, dp_norm_ctas_per_sm(NP)) lars_dp_red
                                                                                     Hyper hy, const float* w,
                                                                                     DpFused f) {
   TRACE_BEGIN
+  pdl_trigger();  // F2's CTAs may be scheduled as F1's retire (they wait in griddepcontrol.wait)
+  pdl_wait();
   // Entry: every rank's gradient for this step is complete once every rank's F1 is running. CTA 0 alone
   // syncs with the other ranks (one LSA barrier instead of one per CTA); the others wait for its go flag.
   // The step epoch cannot move during the entry: the CTA that advances it is the last to finish a tile.
@@ -803,6 +828,7 @@ __global__ void __launch_bounds__(kThreads, dp_norm_ctas_per_sm(NP)) lars_dp_red
   // static tiles (one per CTA): measured faster than 4x finer dynamically scheduled tiles, whose per-tile
   // overhead outweighs the shorter tail (tools/trace_dp.py)
   const bool final_cta = norms_body<CARRY, PeerSumGrad<DT, NP>, false>(wk, sc, hy, w, gl);
+  TRACE_MARK(4)
   if (final_cta || (wk.ntensors == 0 && blockIdx.x == 0 && threadIdx.x == 0)) dp_publish_shares(wk, sc, hy, f);
   __syncthreads();
   TRACE_END(2)
@@ -814,6 +840,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_dp_update_gather_ke
                                                                                      DpFused f) {
   __shared__ int32_t s_status;
   TRACE_BEGIN
+  pdl_trigger();
+  pdl_wait();  // F1 complete (its shares and reduced shard are visible)
   if (threadIdx.x < 32) {
     const int32_t st = dp_collect_shares(wk, sc, hy, f);
     if (threadIdx.x == 0) {
@@ -822,6 +850,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_dp_update_gather_ke
     }
   }
   __syncthreads();
+  TRACE_MARK_AT(4, 0)
   const bool skip = s_status != 0;
   // items ordered last-part-of-every-tile first (see update_item), striped statically over this grid
   if (!skip) {
@@ -861,11 +890,11 @@ template <int DT, bool CARRY>
 static void launch_reduce_norms_np(int np, int grid, cudaStream_t st, const DevWork& wk, const DevScratch& sc,
                                    const Hyper& hy, const float* w, const DpFused& f) {
   if (np <= 2)
-    lars_dp_reduce_norms_kernel<DT, CARRY, 2><<<grid, kThreads, 0, st>>>(wk, sc, hy, w, f);
+    launch_pdl(lars_dp_reduce_norms_kernel<DT, CARRY, 2>, grid, st, wk, sc, hy, w, f);
   else if (np <= 4)
-    lars_dp_reduce_norms_kernel<DT, CARRY, 4><<<grid, kThreads, 0, st>>>(wk, sc, hy, w, f);
+    launch_pdl(lars_dp_reduce_norms_kernel<DT, CARRY, 4>, grid, st, wk, sc, hy, w, f);
   else
-    lars_dp_reduce_norms_kernel<DT, CARRY, 8><<<grid, kThreads, 0, st>>>(wk, sc, hy, w, f);
+    launch_pdl(lars_dp_reduce_norms_kernel<DT, CARRY, 8>, grid, st, wk, sc, hy, w, f);
 }
 
 static void launch_reduce_norms(int32_t dt, bool carry, int np, int grid, cudaStream_t st, const DevWork& wk,
@@ -890,11 +919,11 @@ cudaError_t launch_dp_fused(int32_t dt, const DevWork& wk, const DevScratch& sc,
   if (ev1) cudaEventRecord(ev1, st);
   if (ev2) cudaEventRecord(ev2, st);  // (the exchange now lives inside F1's tail and F2's head)
   if (hy.carry) {
-    if (f.mcast) lars_dp_update_gather_kernel<true, true><<<grid_update, kThreads, 0, st>>>(wg, sc, hy, w, m, f);
-    else lars_dp_update_gather_kernel<true, false><<<grid_update, kThreads, 0, st>>>(wg, sc, hy, w, m, f);
+    if (f.mcast) launch_pdl(lars_dp_update_gather_kernel<true, true>, grid_update, st, wg, sc, hy, w, m, f);
+    else launch_pdl(lars_dp_update_gather_kernel<true, false>, grid_update, st, wg, sc, hy, w, m, f);
   } else {
-    if (f.mcast) lars_dp_update_gather_kernel<false, true><<<grid_update, kThreads, 0, st>>>(wg, sc, hy, w, m, f);
-    else lars_dp_update_gather_kernel<false, false><<<grid_update, kThreads, 0, st>>>(wg, sc, hy, w, m, f);
+    if (f.mcast) launch_pdl(lars_dp_update_gather_kernel<false, true>, grid_update, st, wg, sc, hy, w, m, f);
+    else launch_pdl(lars_dp_update_gather_kernel<false, false>, grid_update, st, wg, sc, hy, w, m, f);
   }
   return cudaGetLastError();
 }
@@ -963,20 +992,6 @@ cudaError_t launch_init_weights(const DevWork& wk, const InitTable& it, float* w
 }
 
 // ---------------------------------------------------------------- launchers
-template <typename K, typename... Args>
-static cudaError_t launch_pdl(K kernel, int grid, cudaStream_t stream, Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kernel, args...);
-}
 
 template <int DT>
 static cudaError_t launch_norms_t(const DevWork& wk, const DevScratch& sc, const Hyper& hy, const float* w,
