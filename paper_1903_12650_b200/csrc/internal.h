@@ -171,6 +171,7 @@ struct DpFused {
   unsigned long long* go;         // F1 entry: CTA 0's "all ranks are in" flag (= epoch + 1)
   unsigned* done;                 // F2 exit: CTAs counted out (the last one syncs with the other ranks)
   bool mcast;                     // NVLS multicast all-gather (multimem.st) instead of per-peer stores
+  int np_template;                // F1 peer-count template bound (>= nranks; 2, 4 or 8)
 };
 // F1 (reduce + norms, grid_norm CTAs), FX (exchange + finish), F2 (update + gather, grid_update CTAs);
 // both grids identical on every rank (the per-CTA LSA barriers pair CTA b with CTA b of every rank).

@@ -915,7 +915,7 @@ cudaError_t launch_dp_fused(int32_t dt, const DevWork& wk, const DevScratch& sc,
                             cudaEvent_t ev2) {
   DevWork wg = wk;
   wg.grid = grid_norm;
-  launch_reduce_norms(dt, hy.carry, f.nranks, grid_norm, st, wg, sc, hy, w, f);
+  launch_reduce_norms(dt, hy.carry, f.np_template, grid_norm, st, wg, sc, hy, w, f);
   if (ev1) cudaEventRecord(ev1, st);
   if (ev2) cudaEventRecord(ev2, st);  // (the exchange now lives inside F1's tail and F2's head)
   if (hy.carry) {

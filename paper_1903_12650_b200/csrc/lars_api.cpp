@@ -177,6 +177,7 @@ struct lars_ctx {
     void* state = nullptr;  // epoch + step iteration
     int grid_norm = 0, grid_update = 0;
     bool mcast = false;
+    int np_template = 0;
   } fused;
   int32_t last_red_dtype = LARS_F16;
   const void* last_red = nullptr;
@@ -282,6 +283,10 @@ static lars_status_t setup_fused(lars_ctx* h) {
     NCCL_OR(ncclDevCommCreate(h->comm, &reqs, &f.dc));
   }
   f.mcast = reqs.lsaMultimem;
+  // F1 is instantiated for up to 2, 4 or 8 peers; LARS_DP_NP (test knob) forces a wider instance so the
+  // P = 8 kernel can be exercised on a box with fewer GPUs (absent peers are predicated off)
+  const char* np_env = getenv("LARS_DP_NP");
+  f.np_template = std::min(8, std::max(h->plan.P, np_env ? atoi(np_env) : 0));
   f.dc_ok = true;
   if (cudaMalloc(&f.gred32, (size_t)h->plan.S * sizeof(float)) != cudaSuccess) return LARS_ERR_OOM;
   if (cudaMalloc(&f.state, 64) != cudaSuccess) return LARS_ERR_OOM;
@@ -671,7 +676,7 @@ static lars_status_t dp_impl(lars_handle_t h, float* w, const void* g, float* m,
               h->rank,       h->plan.P,     begin,          h->fused.gred32,
               (unsigned long long*)h->fused.state, (int64_t*)((char*)h->fused.state + 8),
               (unsigned long long*)((char*)h->fused.state + 16), (unsigned*)((char*)h->fused.state + 24),
-              h->fused.mcast};
+              h->fused.mcast, h->fused.np_template};
     prof_rec(pe, 0, s);
     prof_rec(pe, 1, s);
     CUDA_OR(launch_dp_fused(dt, h->shard.dw, h->shard.sc, hy, w, m, f, h->fused.grid_norm, h->fused.grid_update, s,

@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import json
 import os
+import re
 import sys
 import traceback
 from datetime import timedelta
@@ -172,6 +173,9 @@ def main():
               dict(inject_nan="split", fused=True)),
              ("nan-in-split-layer", LY.skew1b("zipf", n_tensors=50, total=1_000_000), "f16", 100,
               dict(inject_nan="split"))]
+    sel = os.environ.get("DP_CASES")  # optional regex over case names
+    if sel:
+        cases = [c for c in cases if re.search(sel, c[0])]
     for name, lay, dtype, t, kw in cases:
         ok = 1
         try:
