@@ -70,8 +70,17 @@ typedef enum {
   LARS_SHARD_CONTIGUOUS = 0, /* default: layout order, equal shards, <= P-1 layers straddle shard
                                 boundaries (their norms are completed across ranks); the flat layout
                                 (offsets) is the same for every P                                      */
-  LARS_SHARD_LPT = 1         /* whole layers bin-packed (longest processing time): no layer spans ranks,
+  LARS_SHARD_LPT = 1,        /* whole layers bin-packed (longest processing time): no layer spans ranks,
                                 offsets depend on P, padding grows when one layer exceeds ~N/P          */
+  LARS_SHARD_GROUPS = 2      /* static backward-order groups (§III-C-2: "we statically
+                                group layers into several groups beforehand"; sized "several megabytes",
+                                PAPER.md:153): walking the tensors from last to first (the order backward
+                                produces them), a group closes when its gradient bytes first reach
+                                hp.group_bytes; the remaining tensors form the residual group. Every
+                                group's flat span is padded to a multiple of 64*P elements and cut into P
+                                equal slices; rank r owns slice r of EVERY group, so each group is
+                                reduce-scattered on its own as soon as backward has produced it
+                                (dp_group_ready) while the rest of backward runs. NCCL path only.       */
 } lars_shard_policy_t;
 
 /* Gradient wire dtype: fp16 is the paper's; bf16 optional; fp32 allowed. */
@@ -110,6 +119,8 @@ typedef struct {
   int32_t reserved;      /* must be 0                                                             */
   double step_gamma;     /* LARS_DECAY_STEP: factor applied at every milestone (default 0.1)       */
   double milestones[8];  /* LARS_DECAY_STEP: ascending milestones in epochs                        */
+  int64_t group_bytes;   /* LARS_SHARD_GROUPS: gradient bytes (grad_dtype) that close a group
+                            (default 4 MiB, SPEC.md scheduler default; > 0)                         */
 } lars_hparams_t;
 
 /* Learning-rate decay after the warm-up ("step, polynomial, linear"):
@@ -152,7 +163,8 @@ lars_status_t lars_schedule(lars_handle_t h, int64_t* ipe, int64_t* total_iters,
 /* lr(iter) exactly as the kernels use it (double). LARS_ERR_ITER_RANGE outside [0, T). */
 lars_status_t lars_lr_at(lars_handle_t h, int64_t iter, double* lr);
 
-/* Element range [begin, end) of rank `rank`'s shard (P = 1: the whole flat buffer). */
+/* Element range [begin, end) of rank `rank`'s shard (P = 1: the whole flat buffer). Under LARS_SHARD_GROUPS
+ * a rank's elements are not contiguous (slice r of every group, see lars_groups): LARS_ERR_INVALID_ARG. */
 lars_status_t lars_shard_range(lars_handle_t h, int32_t rank, int64_t* begin, int64_t* end);
 
 /* owner[n]: the rank whose shard holds each tensor's first element (a layer that straddles a shard
@@ -168,6 +180,14 @@ lars_status_t lars_tensor_owner(lars_handle_t h, int32_t* owner);
  * key = (seed, 0x4C415253)) for element i of layer l: a pure function of (seed, layer, i), so every rank and
  * every launch configuration produces bitwise the same weights with zero communication. */
 lars_status_t lars_init_weights(lars_handle_t h, float* w, uint64_t seed, void* stream);
+
+/* Static backward-order groups (LARS_SHARD_GROUPS; any other policy reports ONE group = the whole flat buffer).
+ * Group k (k = 0 first: the group backward completes first, i.e. the one holding the LAST tensor) covers flat
+ * elements [begin[k], begin[k] + len[k]) and tensors first_tensor[k] .. last_tensor[k] (inclusive, flat
+ * order); rank r owns [begin[k] + r*len[k]/P, begin[k] + (r+1)*len[k]/P). Call with NULL arrays to get
+ * *ngroups, then with arrays of that many entries (any array may be NULL). */
+lars_status_t lars_groups(lars_handle_t h, int32_t* ngroups, int64_t* begin, int64_t* len, int32_t* first_tensor,
+                          int32_t* last_tensor);
 
 /* Work decomposition of the single-GPU work list (rank < 0) or of a rank's shard: tiles (= CTAs of K1/K2),
  * segments (pieces of layers inside tiles) and warp chunks. Any output may be NULL. */
@@ -212,6 +232,26 @@ lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, cons
 lars_status_t dp_allreduce_lars_step(lars_handle_t h, float* w, const void* g, float* m, int64_t iter,
                                      void* stream);
 
+/* Overlap with backward (LARS_SHARD_GROUPS, NCCL path; "We start to operate allreduce
+ * operation for a part of layers without waiting all layers to be finished ... Allreduce operation is
+ * scheduled as soon as each process finishes backward processing of all layers in a group").
+ * The caller's backward has written every tensor of group `group` into g, ordered on `stream`: the library
+ * starts that group's reduce-scatter on its own communication stream (after an event on `stream`) and
+ * returns; the remaining backward work on `stream` runs concurrently. Groups must be reported in order
+ * 0, 1, 2, ... (every rank then issues the same collective sequence, SPEC.md scheduler) with the same g,
+ * else LARS_ERR_INVALID_ARG. The following dp_allreduce_lars_step (same g) issues the groups not reported
+ * yet, waits for all of them, and finishes the step; its values do not depend on which groups were
+ * reported early. Collective: every rank must report the same groups. */
+lars_status_t dp_group_ready(lars_handle_t h, const void* g, int32_t group, void* stream);
+
+/* Overlap trace (instrumentation for benchmarks and the schedule checker): lars_group_trace_enable(h, 1)
+ * records timing events around every group's reduce-scatter from the next step on. lars_group_trace_read
+ * synchronizes and returns, for the LAST step, milliseconds relative to group 0's ready event:
+ * ready[k] (dp_group_ready or, for groups issued by the step itself, the step call), rs_start[k], rs_end[k]
+ * (n = ngroups entries each) and *applied (the step's end on the caller's stream). Arrays may be NULL. */
+lars_status_t lars_group_trace_enable(lars_handle_t h, int32_t enable);
+lars_status_t lars_group_trace_read(lars_handle_t h, double* ready, double* rs_start, double* rs_end, double* applied);
+
 /* dp_allreduce_lars_step with the iteration in device memory (see lars_step_dev_iter). */
 lars_status_t dp_allreduce_lars_step_dev_iter(lars_handle_t h, float* w, const void* g, float* m, int64_t* iter_dev,
                                               void* stream);
@@ -243,7 +283,9 @@ lars_status_t lars_profile_read(lars_handle_t h, double* ms, int64_t* steps);
 lars_status_t lars_dp_buffers(lars_handle_t h, float** w, void** g);
 
 /* Device pointer to the reduced gradient shard of the last dp step (S elements of *dtype: the wire dtype on
- * the NCCL path, LARS_F32 on the fused path; first element = global element `begin`). Owned by the library. */
+ * the NCCL path, LARS_F32 on the fused path; first element = global element `begin`). Owned by the library.
+ * Under LARS_SHARD_GROUPS the buffer is flat (begin = 0, end = padded_numel) and only this rank's slices of
+ * every group hold reduced values. */
 lars_status_t lars_reduced_grad(lars_handle_t h, const void** dev_ptr, int32_t* dtype, int64_t* begin, int64_t* end);
 
 /* Synchronizing readbacks of the last step (per tensor; entries of tensors this rank does not own are

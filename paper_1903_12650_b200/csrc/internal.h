@@ -91,6 +91,14 @@ struct Plan {
   int64_t ipe = 0, T = 0, W = 0;
   std::vector<double> lr;       // lr[t], t in [0, T)
   uint64_t hash = 0;
+  // static backward-order groups (LARS_SHARD_GROUPS; otherwise one group = the whole flat buffer)
+  int32_t policy = LARS_SHARD_CONTIGUOUS;
+  struct Group {
+    int64_t begin = 0, len = 0;  // flat span, len a multiple of 64*P
+    int32_t first = 0, last = 0; // tensors first..last (flat order)
+  };
+  std::vector<Group> groups;     // k = 0: the group backward completes first (holds the last tensor)
+  std::vector<int32_t> group_of; // tensor -> group
 };
 
 lars_status_t validate_hparams(const lars_hparams_t& hp);

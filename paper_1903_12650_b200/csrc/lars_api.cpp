@@ -190,6 +190,12 @@ struct lars_ctx {
   std::vector<cudaEvent_t> ev;
   void* init_mem = nullptr;  // InitTable of the whole-layout work list (lars_init_weights)
   InitTable init{};
+  // static backward-order groups (LARS_SHARD_GROUPS): reduce-scatter of group k on cs as soon as the
+  // caller reports it (dp_group_ready); the step issues the rest. Events: ready/rs_start/rs_end per group.
+  int32_t next_group = 0;
+  const void* group_g = nullptr;
+  std::vector<cudaEvent_t> gev;  // [3*G + 2]: ready[k], rs0[k], rs1[k], then rs_all_done, applied
+  bool gtrace = false, gtrace_valid = false;
 };
 
 // Tile-aligned buckets of ~equal element counts for every rank (the plan is static: every rank derives
@@ -251,6 +257,7 @@ static bool fused_eligible(lars_ctx* h) {
   const char* env = getenv("LARS_DP_FUSED");
   if (env && env[0] == '0') return false;
   if (h->plan.P > 8) return false;  // kMaxRanks
+  if (h->plan.policy == LARS_SHARD_GROUPS) return false;  // per-group slices: NCCL path
   return ncclTeamLsa(h->comm).nRanks == h->plan.P;  // every rank on one NVLink domain
 }
 
@@ -322,6 +329,7 @@ void lars_hparams_default(lars_hparams_t* hp) {
   hp->nranks = 1;
   hp->tile_elems = 0;
   hp->step_gamma = 0.1;
+  hp->group_bytes = (int64_t)4 << 20;
 }
 
 const char* lars_version(void) { return "lars-b200 0.1 (sm_100a)"; }
@@ -398,8 +406,23 @@ lars_status_t lars_lr_at(lars_handle_t h, int64_t iter, double* lr) {
 
 lars_status_t lars_shard_range(lars_handle_t h, int32_t rank, int64_t* begin, int64_t* end) {
   if (!h || rank < 0 || rank >= h->plan.P) return LARS_ERR_INVALID_ARG;
+  if (h->plan.policy == LARS_SHARD_GROUPS && h->plan.P > 1) return LARS_ERR_INVALID_ARG;  // not contiguous
   if (begin) *begin = (int64_t)rank * h->plan.S;
   if (end) *end = (int64_t)(rank + 1) * h->plan.S;
+  return LARS_OK;
+}
+
+lars_status_t lars_groups(lars_handle_t h, int32_t* ngroups, int64_t* begin, int64_t* len, int32_t* first_tensor,
+                          int32_t* last_tensor) {
+  if (!h || !ngroups) return LARS_ERR_INVALID_ARG;
+  const auto& G = h->plan.groups;
+  *ngroups = (int32_t)G.size();
+  for (size_t k = 0; k < G.size(); ++k) {
+    if (begin) begin[k] = G[k].begin;
+    if (len) len[k] = G[k].len;
+    if (first_tensor) first_tensor[k] = G[k].first;
+    if (last_tensor) last_tensor[k] = G[k].last;
+  }
   return LARS_OK;
 }
 
@@ -588,8 +611,15 @@ lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, cons
   }
   lars_status_t st = upload(h->shard, h->sms, h->plan.nsplit, true);
   if (st != LARS_OK) return st;
-  if (cudaMalloc(&h->gred, (size_t)h->plan.S * dtype_size(h->hp.grad_dtype)) != cudaSuccess) return LARS_ERR_OOM;
-  CUDA_OR(cudaMemset(h->gred, 0, (size_t)h->plan.S * dtype_size(h->hp.grad_dtype)));
+  // reduced gradient: the rank's shard, or (groups) a flat buffer whose slices of every group are this rank's
+  const size_t red_elems = (size_t)(h->plan.policy == LARS_SHARD_GROUPS ? h->plan.padded : h->plan.S);
+  if (cudaMalloc(&h->gred, red_elems * dtype_size(h->hp.grad_dtype)) != cudaSuccess) return LARS_ERR_OOM;
+  CUDA_OR(cudaMemset(h->gred, 0, red_elems * dtype_size(h->hp.grad_dtype)));
+  if (h->plan.policy == LARS_SHARD_GROUPS) {
+    CUDA_OR(cudaStreamCreateWithFlags(&h->cs, cudaStreamNonBlocking));
+    h->gev.assign(3 * h->plan.groups.size() + 2, nullptr);
+    for (auto& e : h->gev) CUDA_OR(cudaEventCreate(&e));  // timing events (also used for ordering)
+  }
   h->shard_ready = true;
   if (fused) {
     st = setup_fused(h);
@@ -662,6 +692,109 @@ static lars_status_t dp_bucketed(lars_handle_t h, float* w, const void* g, float
   return LARS_OK;
 }
 
+// Static-group schedule (LARS_SHARD_GROUPS). Communication stream cs: reduce-scatter of group k into this
+// rank's slice of the flat gred buffer, in group order, each after the caller's ready event for k
+// (dp_group_ready) or the step's own. Caller's stream s: K1 over every slice, C3 + finisher, K2, then one
+// grouped all-gather (in place, per group) — the values are those of K = 1 up to NCCL's reduction order.
+static lars_status_t issue_group(lars_handle_t h, const void* g, int32_t k, cudaStream_t s) {
+  const auto& G = h->plan.groups[k];
+  const int32_t P = h->plan.P, dt = h->hp.grad_dtype;
+  const size_t esz = dtype_size(dt);
+  const int64_t c = G.len / P;
+  const int32_t ng = (int32_t)h->plan.groups.size();
+  CUDA_OR(cudaEventRecord(h->gev[k], s));  // ready[k]: the caller's backward wrote every member of group k
+  CUDA_OR(cudaStreamWaitEvent(h->cs, h->gev[k], 0));
+  if (h->gtrace) CUDA_OR(cudaEventRecord(h->gev[ng + k], h->cs));
+  NCCL_OR(ncclReduceScatter((const char*)g + G.begin * esz, (char*)h->gred + (G.begin + h->rank * c) * esz,
+                            (size_t)c, nccl_type(dt), ncclSum, h->comm, h->cs));
+  if (h->gtrace) CUDA_OR(cudaEventRecord(h->gev[2 * ng + k], h->cs));
+  return LARS_OK;
+}
+
+static lars_status_t dp_groups(lars_handle_t h, float* w, const void* g, float* m, const Hyper& hy, cudaStream_t s,
+                               std::array<cudaEvent_t, 6>* pe) {
+  const int32_t ng = (int32_t)h->plan.groups.size(), P = h->plan.P, dt = h->hp.grad_dtype;
+  if (h->next_group > 0 && g != h->group_g) return LARS_ERR_INVALID_ARG;  // early groups used another g
+  prof_rec(pe, 0, s);
+  for (int32_t k = h->next_group; k < ng; ++k) {
+    lars_status_t st = issue_group(h, g, k, s);
+    if (st != LARS_OK) return st;
+  }
+  h->next_group = 0;
+  h->group_g = nullptr;
+  CUDA_OR(cudaEventRecord(h->gev[3 * ng], h->cs));
+  CUDA_OR(cudaStreamWaitEvent(s, h->gev[3 * ng], 0));
+  prof_rec(pe, 1, s);
+  CUDA_OR(launch_norms(dt, h->shard.dw, h->shard.sc, hy, w, h->gred, 0, s));                       // K1
+  prof_rec(pe, 2, s);
+  NCCL_OR(ncclAllReduce(h->shard.sc.c3, h->shard.sc.c3, 1 + 2 * (size_t)h->plan.nsplit, ncclFloat64, ncclSum,
+                        h->comm, s));                                                             // C3
+  CUDA_OR(launch_split_finish(h->shard.dw, h->shard.sc, hy, s));
+  prof_rec(pe, 3, s);
+  CUDA_OR(launch_update(dt, h->shard.dw, h->shard.sc, hy, w, h->gred, 0, m, s));                   // K2
+  prof_rec(pe, 4, s);
+  NCCL_OR(ncclGroupStart());
+  for (const auto& G : h->plan.groups) {                                                           // C2
+    const int64_t c = G.len / P;
+    NCCL_OR(ncclAllGather(w + G.begin + h->rank * c, w + G.begin, (size_t)c, ncclFloat32, h->comm, s));
+  }
+  NCCL_OR(ncclGroupEnd());
+  prof_rec(pe, 5, s);
+  CUDA_OR(cudaEventRecord(h->gev[3 * ng + 1], s));  // applied
+  h->gtrace_valid = h->gtrace;
+  h->last_stream = s;
+  h->last = &h->shard;
+  h->last_red = h->gred;
+  h->last_red_dtype = dt;
+  return LARS_OK;
+}
+
+lars_status_t dp_group_ready(lars_handle_t h, const void* g, int32_t group, void* stream) {
+  if (!h || !g) return LARS_ERR_INVALID_ARG;
+  if (h->device < 0) return LARS_ERR_NO_DEVICE;
+  if (!h->comm || !h->shard_ready) return LARS_ERR_NO_COMM;
+  if (h->plan.policy != LARS_SHARD_GROUPS) return LARS_ERR_INVALID_ARG;
+  if (group != h->next_group || group >= (int32_t)h->plan.groups.size()) return LARS_ERR_INVALID_ARG;
+  if (group > 0 && g != h->group_g) return LARS_ERR_INVALID_ARG;
+  if ((uintptr_t)g & 255u) return LARS_ERR_ALIGNMENT;
+  DeviceGuard dg(h->device);
+  lars_status_t st = issue_group(h, g, group, (cudaStream_t)stream);
+  if (st != LARS_OK) return st;
+  h->group_g = g;
+  h->next_group = group + 1;
+  return LARS_OK;
+}
+
+lars_status_t lars_group_trace_enable(lars_handle_t h, int32_t enable) {
+  if (!h) return LARS_ERR_INVALID_ARG;
+  if (h->plan.policy != LARS_SHARD_GROUPS || h->gev.empty()) return LARS_ERR_NO_COMM;
+  h->gtrace = enable != 0;
+  h->gtrace_valid = false;
+  return LARS_OK;
+}
+
+lars_status_t lars_group_trace_read(lars_handle_t h, double* ready, double* rs_start, double* rs_end, double* applied) {
+  if (!h) return LARS_ERR_INVALID_ARG;
+  if (!h->gtrace_valid) return LARS_ERR_NO_COMM;
+  DeviceGuard dg(h->device);
+  const int32_t ng = (int32_t)h->plan.groups.size();
+  CUDA_OR(cudaEventSynchronize(h->gev[3 * ng + 1]));
+  auto rel = [&](cudaEvent_t e, double* out) -> lars_status_t {
+    float ms = 0.f;
+    CUDA_OR(cudaEventElapsedTime(&ms, h->gev[0], e));
+    *out = ms;
+    return LARS_OK;
+  };
+  for (int32_t k = 0; k < ng; ++k) {
+    lars_status_t st = LARS_OK;
+    if (ready && (st = rel(h->gev[k], ready + k)) != LARS_OK) return st;
+    if (rs_start && (st = rel(h->gev[ng + k], rs_start + k)) != LARS_OK) return st;
+    if (rs_end && (st = rel(h->gev[2 * ng + k], rs_end + k)) != LARS_OK) return st;
+  }
+  if (applied) return rel(h->gev[3 * ng + 1], applied);
+  return LARS_OK;
+}
+
 static lars_status_t dp_impl(lars_handle_t h, float* w, const void* g, float* m, const Hyper& hy, void* stream) {
   if (!h->comm || !h->shard_ready) return LARS_ERR_NO_COMM;
   DeviceGuard dg(h->device);
@@ -693,6 +826,7 @@ static lars_status_t dp_impl(lars_handle_t h, float* w, const void* g, float* m,
     return LARS_OK;
   }
   if (h->K > 1) return dp_bucketed(h, w, g, m, hy, s, pe);
+  if (h->plan.policy == LARS_SHARD_GROUPS) return dp_groups(h, w, g, m, hy, s, pe);
   prof_rec(pe, 0, s);
   NCCL_OR(ncclReduceScatter(g, h->gred, (size_t)S, nccl_type(dt), ncclSum, h->comm, s));          // C1
   prof_rec(pe, 1, s);
@@ -831,8 +965,9 @@ lars_status_t lars_reduced_grad(lars_handle_t h, const void** dev_ptr, int32_t* 
   if (!h->gred) return LARS_ERR_NO_COMM;
   *dev_ptr = h->last_red ? h->last_red : h->gred;
   if (dtype) *dtype = h->last_red ? h->last_red_dtype : h->hp.grad_dtype;
-  if (begin) *begin = (int64_t)h->rank * h->plan.S;
-  if (end) *end = (int64_t)(h->rank + 1) * h->plan.S;
+  const bool flat = h->plan.policy == LARS_SHARD_GROUPS && h->last_red == h->gred;
+  if (begin) *begin = flat ? 0 : (int64_t)h->rank * h->plan.S;
+  if (end) *end = flat ? h->plan.padded : (int64_t)(h->rank + 1) * h->plan.S;
   return LARS_OK;
 }
 
@@ -894,6 +1029,8 @@ lars_status_t lars_destroy(lars_handle_t h) {
       cudaFree(f.gred32);
       cudaFree(f.state);
       for (auto e : h->ev)
+        if (e) cudaEventDestroy(e);
+      for (auto e : h->gev)
         if (e) cudaEventDestroy(e);
       if (h->cs) cudaStreamDestroy(h->cs);
       ncclCommDestroy(h->comm);

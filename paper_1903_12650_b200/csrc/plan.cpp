@@ -30,6 +30,7 @@ lars_status_t validate_hparams(const lars_hparams_t& hp) {
   if (hp.nranks < 1 || hp.nranks > 4096) return LARS_ERR_INVALID_ARG;
   if (hp.tile_elems < 0) return LARS_ERR_INVALID_ARG;
   if (hp.buckets < 0 || hp.buckets > 1024 || hp.reserved != 0) return LARS_ERR_INVALID_ARG;
+  if (hp.shard_policy == LARS_SHARD_GROUPS && (hp.group_bytes <= 0 || hp.buckets > 1)) return LARS_ERR_INVALID_ARG;
   if (hp.decay != LARS_DECAY_POLY && hp.decay != LARS_DECAY_STEP) return LARS_ERR_INVALID_ARG;
   if (hp.flags & ~(LARS_FLAG_CARRY_WNORM | LARS_FLAG_LR_AT_APPLY)) return LARS_ERR_INVALID_ARG;
   if (hp.decay == LARS_DECAY_STEP) {
@@ -80,7 +81,51 @@ static lars_status_t make_schedule(const lars_hparams_t& hp, Plan& p) {
 // P > 1 with LARS_SHARD_LPT: whole-tensor longest-processing-time bin packing (ties: larger tensor
 //   first, then lower index; equal loads -> lower rank), rank-major, tensors inside a shard in index
 //   order; no layer spans ranks (SURVEY.md §8(e) "D1"), padding grows when a layer exceeds ~N/P.
-static void make_layout(Plan& p, int32_t policy) {
+// P >= 1 with LARS_SHARD_GROUPS (SPEC.md make_buckets): greedy in backward order (last
+//   tensor first), a group closes when its gradient bytes first reach group_bytes, the tail is the
+//   residual group. Tensors keep flat order inside and across groups; each group's span is padded to a
+//   multiple of 64*P and rank r owns slice r of every group. A tensor crossing a slice boundary is split.
+static void make_groups_layout(Plan& p, const std::vector<int64_t>& asz, int64_t group_bytes, int32_t esz) {
+  const int32_t L = p.L, P = p.P;
+  std::vector<std::pair<int32_t, int32_t>> ranges;  // (first, last) in backward order
+  int64_t acc = 0;
+  int32_t last = L - 1;
+  for (int32_t l = L - 1; l >= 0; --l) {
+    acc += p.numel[l] * esz;
+    if (acc >= group_bytes || l == 0) {
+      ranges.push_back({l, last});
+      last = l - 1;
+      acc = 0;
+    }
+  }
+  const int32_t G = (int32_t)ranges.size();
+  p.groups.assign(G, Plan::Group{});
+  p.group_of.assign(L, 0);
+  int64_t off = 0;
+  for (int32_t k = G - 1; k >= 0; --k) {  // flat order = reverse backward order
+    Plan::Group& g = p.groups[k];
+    g.first = ranges[k].first;
+    g.last = ranges[k].second;
+    g.begin = off;
+    for (int32_t l = g.first; l <= g.last; ++l) {
+      p.offset[l] = off;
+      p.group_of[l] = k;
+      off += asz[l];
+    }
+    g.len = round_up(off - g.begin, kAlign * P);
+    off = g.begin + g.len;
+  }
+  p.padded = off;
+  p.S = off / P;  // elements per rank (sum of its slices)
+  for (int32_t l = 0; l < L; ++l) {
+    const Plan::Group& g = p.groups[p.group_of[l]];
+    const int64_t c = g.len / P;
+    p.owner[l] = (int32_t)((p.offset[l] - g.begin) / c);
+    if ((p.offset[l] + p.numel[l] - 1 - g.begin) / c != (p.offset[l] - g.begin) / c) p.split[l] = p.nsplit++;
+  }
+}
+
+static void make_layout(Plan& p, int32_t policy, int64_t group_bytes, int32_t esz) {
   const int32_t L = p.L, P = p.P;
   std::vector<int64_t> asz(L);
   for (int32_t l = 0; l < L; ++l) asz[l] = round_up(p.numel[l], kAlign);
@@ -88,6 +133,11 @@ static void make_layout(Plan& p, int32_t policy) {
   p.offset.assign(L, 0);
   p.split.assign(L, -1);
   p.nsplit = 0;
+  p.policy = policy;
+  if (policy == LARS_SHARD_GROUPS) {
+    make_groups_layout(p, asz, group_bytes, esz);
+    return;
+  }
   if (P == 1 || policy == LARS_SHARD_CONTIGUOUS) {
     int64_t off = 0;
     for (int32_t l = 0; l < L; ++l) { p.offset[l] = off; off += asz[l]; }
@@ -129,7 +179,9 @@ static uint64_t fnv1a(uint64_t h, const void* data, size_t n) {
 }
 
 lars_status_t make_plan(const lars_tensor_t* t, int32_t n, const lars_hparams_t& hp, Plan& p) {
-  if (hp.shard_policy != LARS_SHARD_CONTIGUOUS && hp.shard_policy != LARS_SHARD_LPT) return LARS_ERR_INVALID_ARG;
+  if (hp.shard_policy != LARS_SHARD_CONTIGUOUS && hp.shard_policy != LARS_SHARD_LPT &&
+      hp.shard_policy != LARS_SHARD_GROUPS)
+    return LARS_ERR_INVALID_ARG;
   if (n <= 0 || t == nullptr) return LARS_ERR_LAYOUT;
   lars_status_t st = validate_hparams(hp);
   if (st != LARS_OK) return st;
@@ -148,7 +200,12 @@ lars_status_t make_plan(const lars_tensor_t* t, int32_t n, const lars_hparams_t&
   }
   st = make_schedule(hp, p);
   if (st != LARS_OK) return st;
-  make_layout(p, hp.shard_policy);
+  const int32_t esz = hp.grad_dtype == LARS_F32 ? 4 : 2;
+  make_layout(p, hp.shard_policy, hp.group_bytes, esz);
+  if (p.groups.empty()) {  // every other policy: one group, the whole flat buffer
+    p.groups.assign(1, Plan::Group{0, p.padded, 0, p.L - 1});
+    p.group_of.assign(p.L, 0);
+  }
   uint64_t h = 1469598103934665603ull;
   h = fnv1a(h, &p.L, sizeof p.L);
   h = fnv1a(h, &p.P, sizeof p.P);
@@ -159,7 +216,8 @@ lars_status_t make_plan(const lars_tensor_t* t, int32_t n, const lars_hparams_t&
   const double hd[] = {hp.base_lr, hp.eta, hp.momentum, hp.weight_decay, hp.eps, hp.warmup_epochs,
                        hp.poly_power, hp.grad_scale, hp.step_gamma, (double)hp.decay, (double)hp.flags};
   h = fnv1a(h, hd, sizeof hd);
-  const int64_t hi[] = {hp.global_batch, hp.dataset_size, hp.total_epochs, hp.grad_dtype, hp.shard_policy};
+  const int64_t hi[] = {hp.global_batch, hp.dataset_size, hp.total_epochs, hp.grad_dtype, hp.shard_policy,
+                        hp.shard_policy == LARS_SHARD_GROUPS ? hp.group_bytes : 0};
   h = fnv1a(h, hi, sizeof hi);
   h = fnv1a(h, p.lr.data(), p.lr.size() * sizeof(double));  // the whole schedule, milestones included
   p.hash = h;
@@ -177,7 +235,12 @@ static void piece(const Plan& p, int32_t l, int32_t rank, int64_t& lo, int64_t& 
   lo = 0;
   hi = p.numel[l];
   if (rank < 0) return;
-  const int64_t b = (int64_t)rank * p.S, e = b + p.S;
+  int64_t b = (int64_t)rank * p.S, e = b + p.S;
+  if (p.policy == LARS_SHARD_GROUPS) {  // slice `rank` of the tensor's group
+    const Plan::Group& g = p.groups[p.group_of[l]];
+    b = g.begin + rank * (g.len / p.P);
+    e = b + g.len / p.P;
+  }
   lo = std::max<int64_t>(0, b - p.offset[l]);
   hi = std::min<int64_t>(p.numel[l], e - p.offset[l]);
 }

@@ -22,7 +22,7 @@ HEADER = os.path.join(os.path.dirname(PKG), "include", "lars.h")
 KIND = {"weight": 0, "bias": 1, "bn_gamma": 2, "bn_beta": 3}
 DTYPE = {"f32": 0, "f16": 1, "bf16": 2}
 DTYPE_BYTES = {"f32": 4, "f16": 2, "bf16": 2}
-SHARD_POLICY = {"contiguous": 0, "lpt": 1}
+SHARD_POLICY = {"contiguous": 0, "lpt": 1, "groups": 2}
 DECAY = {"poly": 0, "step": 1}
 FLAG_CARRY_WNORM = 1
 FLAG_LR_AT_APPLY = 2
@@ -49,7 +49,7 @@ class HParams(ctypes.Structure):
                 ("total_epochs", c_int32), ("grad_dtype", c_int32), ("nranks", c_int32),
                 ("tile_elems", c_int32), ("shard_policy", c_int32), ("flags", ctypes.c_uint32),
                 ("buckets", c_int32), ("decay", c_int32), ("n_milestones", c_int32), ("reserved", c_int32),
-                ("step_gamma", c_double), ("milestones", c_double * 8)]
+                ("step_gamma", c_double), ("milestones", c_double * 8), ("group_bytes", c_int64)]
 
 
 _lib = None
@@ -87,6 +87,12 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "lars_profile_read": (c_int32, [h, POINTER(c_double), POINTER(c_int64)]),
         "lars_reduced_grad": (c_int32, [h, POINTER(c_void_p), POINTER(c_int32), POINTER(c_int64), POINTER(c_int64)]),
         "lars_dp_buffers": (c_int32, [h, POINTER(c_void_p), POINTER(c_void_p)]),
+        "lars_groups": (c_int32, [h, POINTER(c_int32), POINTER(c_int64), POINTER(c_int64), POINTER(c_int32),
+                                  POINTER(c_int32)]),
+        "dp_group_ready": (c_int32, [h, c_void_p, c_int32, c_void_p]),
+        "lars_group_trace_enable": (c_int32, [h, c_int32]),
+        "lars_group_trace_read": (c_int32, [h, POINTER(c_double), POINTER(c_double), POINTER(c_double),
+                                            POINTER(c_double)]),
         "lars_last_norms": (c_int32, [h, POINTER(c_double), POINTER(c_double), POINTER(c_double),
                                       POINTER(c_double)]),
         "lars_last_step_skipped": (c_int32, [h, POINTER(c_int32)]),
@@ -216,6 +222,16 @@ class Lars:
         _check(self._lib.lars_shard_range(self._h, rank, byref(b), byref(e)), "lars_shard_range")
         return int(b.value), int(e.value)
 
+    def groups(self) -> list[dict]:
+        """Static backward-order groups: k = 0 is the group backward completes first (LARS_SHARD_GROUPS;
+        any other policy: one group covering the whole flat buffer)."""
+        n = c_int32()
+        _check(self._lib.lars_groups(self._h, byref(n), None, None, None, None), "lars_groups")
+        G = int(n.value)
+        b, ln, f, l = (c_int64 * G)(), (c_int64 * G)(), (c_int32 * G)(), (c_int32 * G)()
+        _check(self._lib.lars_groups(self._h, byref(n), b, ln, f, l), "lars_groups")
+        return [{"begin": int(b[k]), "len": int(ln[k]), "first": int(f[k]), "last": int(l[k])} for k in range(G)]
+
     def tensor_owner(self) -> list[int]:
         o = (c_int32 * self.n)()
         _check(self._lib.lars_tensor_owner(self._h, o), "lars_tensor_owner")
@@ -276,6 +292,20 @@ class Lars:
                "dp_allreduce_lars_step")
 
     dp_step = dp_allreduce_lars_step
+
+    def dp_group_ready(self, g, group: int, stream=None) -> None:
+        """Backward has written every tensor of `group` into g (ordered on `stream`): start its reduction."""
+        _check(self._lib.dp_group_ready(self._h, _ptr(g), group, _stream(stream)), "dp_group_ready")
+
+    def group_trace_enable(self, on: bool = True) -> None:
+        _check(self._lib.lars_group_trace_enable(self._h, 1 if on else 0), "lars_group_trace_enable")
+
+    def group_trace_read(self) -> dict:
+        """Last step, ms relative to group 0's ready event: ready/rs_start/rs_end per group, applied."""
+        G = len(self.groups())
+        r, a, b, ap = (c_double * G)(), (c_double * G)(), (c_double * G)(), c_double()
+        _check(self._lib.lars_group_trace_read(self._h, r, a, b, byref(ap)), "lars_group_trace_read")
+        return {"ready": list(r), "rs_start": list(a), "rs_end": list(b), "applied": ap.value}
 
     def dp_allreduce_lars_step_host_grad(self, w, g_host, m, it: int, stream=None) -> None:
         _check(self._lib.dp_allreduce_lars_step_host_grad(self._h, _ptr(w), _ptr(g_host), _ptr(m), it,

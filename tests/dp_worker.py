@@ -48,9 +48,35 @@ def main():
         dist.all_reduce(hi, op=dist.ReduceOp.MAX)
         return bool(torch.equal(lo, hi))
 
-    def run_case(name, lay, dtype, t, kind="random", inject_nan=False, fused=False, **hpkw):
+    def owned_ranges(h, r):
+        """Flat element ranges rank r reduces and updates (one shard, or slice r of every static group)."""
+        if hpkw_policy(h) == "groups":
+            return [(gk["begin"] + r * (gk["len"] // P), gk["begin"] + (r + 1) * (gk["len"] // P))
+                    for gk in h.groups()]
+        return [h.shard_range(r)]
+
+    def hpkw_policy(h):
+        return getattr(h, "_policy", "contiguous")
+
+    def backward_then_ready(h, g_src, g, early):
+        """Synthetic backward: tensors written into g in backward order (last tensor first), each after a
+        short device spin; group k is reported (dp_group_ready) right after its last member is written.
+        early = number of groups reported before the step (the step issues the rest)."""
+        groups = h.groups()
+        g.zero_()
+        for k, gk in enumerate(groups):
+            for l in range(gk["last"], gk["first"] - 1, -1):
+                torch.cuda._sleep(2000)
+                o, n = h.offsets[l], h.sizes[l]
+                g[o:o + n].copy_(g_src[o:o + n])
+            if k < early:
+                h.dp_group_ready(g, k)
+
+    def run_case(name, lay, dtype, t, kind="random", inject_nan=False, fused=False, overlap=None, **hpkw):
         kw = hp_kwargs(grad_dtype=dtype, grad_scale=1.0 / (G.GRAD_PRESCALE * P), **hpkw)
         h = PK.Lars([(x.numel, x.kind) for x in lay], device=local, nranks=P, **kw)
+        h._policy = kw.get("shard_policy", "contiguous")
+        h.sizes = [x.numel for x in lay]
         h.comm_init_torch()
         w_l, m_l = G.weights(lay), G.momentum(lay, 1e-3)
         if kind == "integer":
@@ -60,8 +86,10 @@ def main():
         if inject_nan:  # rank 1 poisons one element of ITS local gradient
             q, l0, i0 = 1 % P, 0, 3
             if inject_nan == "split":  # ... the last element of a layer that straddles a shard boundary
-                S = h.padded_numel // P
-                l0 = next(l for l, x in enumerate(lay) if h.offsets[l] // S != (h.offsets[l] + x.numel - 1) // S)
+                rng0 = owned_ranges(h, 0) + owned_ranges(h, 1 % P)
+                cuts = sorted({e for _, e in rng0} | {b for b, _ in rng0})
+                l0 = next(l for l, x in enumerate(lay)
+                          if any(h.offsets[l] < c < h.offsets[l] + x.numel for c in cuts))
                 i0 = lay[l0].numel - 1
             g_all[q][l0] = g_all[q][l0].copy()
             g_all[q][l0][i0] = np.nan
@@ -75,9 +103,28 @@ def main():
             w, g = w_sym, g_sym
             torch.cuda.synchronize()
         g_before = g.clone()
+        if overlap:  # static groups reported while the synthetic backward still runs
+            ng = len(h.groups())
+            assert ng > 1, f"{name}: expected several groups"
+            try:  # out-of-order report is rejected before anything is enqueued
+                h.dp_group_ready(g, 1)
+                raise AssertionError("out-of-order group accepted")
+            except PK.LarsError as e:
+                assert e.status == 1, e
+            h.group_trace_enable(True)
+            backward_then_ready(h, g_before, g, ng if overlap == "all" else ng // 2)
         h.dp_allreduce_lars_step(w, g, m, t)
         torch.cuda.synchronize()
         res = {"name": name, "dtype": dtype, "t": t}
+        if overlap:
+            tr = h.group_trace_read()
+            ng = len(tr["ready"])
+            eps = 2e-3  # event timer resolution (ms)
+            assert all(tr["rs_start"][k] + eps >= tr["ready"][k] for k in range(ng)), tr
+            assert all(tr["rs_start"][k] + eps >= tr["rs_end"][k - 1] for k in range(1, ng)), tr
+            assert tr["applied"] + eps >= max(tr["rs_end"]), tr
+            res["groups"] = ng
+            res["first_rs_before_backward_end_ms"] = round(tr["ready"][-1] - tr["rs_start"][0], 4)
         same = all_same(w)  # collectives first: every rank calls them before any rank-local assertion
         red_t, b, e = h.reduced_grad()
         red_dtype = {torch.float32: "f32", torch.float16: "f16", torch.int16: "bf16"}[red_t.dtype]
@@ -85,7 +132,15 @@ def main():
             red_t = red_t.view(torch.float16)
         parts = [torch.empty_like(red_t) for _ in range(P)]
         dist.all_gather(parts, red_t.clone())
-        full_red = from_dev(torch.cat(parts))  # the exact buffer every K1 read, all shards
+        if hpkw_policy(h) == "groups":  # flat buffers: rank r's slices come from rank r
+            full_red = np.zeros(h.padded_numel, dtype=from_dev(parts[0][:1]).dtype)
+            for r in range(P):
+                pr = from_dev(parts[r])
+                for lo, hi in owned_ranges(h, r):
+                    full_red[lo:hi] = pr[lo:hi]
+            b, e = 0, h.padded_numel
+        else:
+            full_red = from_dev(torch.cat(parts))  # the exact buffer every K1 read, all shards
         if red_dtype == "bf16":
             full_red = full_red.view(np.uint16)
         res["reduced_dtype"] = red_dtype
@@ -97,10 +152,12 @@ def main():
         sizes = [x.numel for x in lay]
         # this rank's piece of every layer (layers may straddle shard boundaries)
         pieces = {}
-        for l in range(len(lay)):
-            lo, hi = max(h.offsets[l], b), min(h.offsets[l] + sizes[l], e)
-            if hi > lo:
-                pieces[l] = (lo - h.offsets[l], hi - h.offsets[l])
+        for rb, re_ in owned_ranges(h, rank):
+            for l in range(len(lay)):
+                lo, hi = max(h.offsets[l], rb), min(h.offsets[l] + sizes[l], re_)
+                if hi > lo:
+                    assert l not in pieces, "a layer meets one rank in one piece"
+                    pieces[l] = (lo - h.offsets[l], hi - h.offsets[l])
         mine = sorted(pieces)
         res["split_layers_here"] = sum(1 for l in mine if pieces[l] != (0, sizes[l]))
         wg = G.unpack(from_dev(w), h.offsets, sizes)
@@ -172,7 +229,17 @@ def main():
              ("fused-nan-in-split-layer", LY.skew1b("zipf", n_tensors=50, total=1_000_000), "f16", 100,
               dict(inject_nan="split", fused=True)),
              ("nan-in-split-layer", LY.skew1b("zipf", n_tensors=50, total=1_000_000), "f16", 100,
-              dict(inject_nan="split"))]
+              dict(inject_nan="split")),
+             # static backward-order groups (NEXT-f2)
+             ("groups-r50-f16", lay_r50, "f16", 719, dict(shard_policy="groups", group_bytes=4 << 20)),
+             ("groups-r50-int-overlap", lay_r50, "f16", 80, dict(kind="integer", shard_policy="groups",
+                                                                 group_bytes=4 << 20, overlap="all")),
+             ("groups-random-bf16-overlap-half", LY.random_layout(np.random.default_rng(8), 29), "bf16", 700,
+              dict(shard_policy="groups", group_bytes=64 << 10, overlap="half")),
+             ("groups-zipf-f32-carry-overlap", LY.skew1b("zipf", n_tensors=200, total=4_000_000), "f32", 500,
+              dict(shard_policy="groups", group_bytes=1 << 20, flags=1, overlap="all")),
+             ("groups-nan-in-split-layer", LY.skew1b("zipf", n_tensors=50, total=1_000_000), "f16", 100,
+              dict(inject_nan="split", shard_policy="groups", group_bytes=256 << 10, overlap="all"))]
     sel = os.environ.get("DP_CASES")  # optional regex over case names
     if sel:
         cases = [c for c in cases if re.search(sel, c[0])]

@@ -19,7 +19,7 @@ def _free_port() -> int:
     return p
 
 
-def _worker(rank, world, port, errors):
+def _worker(rank, world, port, errors, policy="contiguous"):
     import torch
     import torch.distributed as dist
 
@@ -32,7 +32,8 @@ def _worker(rank, world, port, errors):
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=world)
         lay = LY.resnet50()[:45] + LY.random_layout(np.random.default_rng(3), 20)
-        kw = dict(base_lr=32.0, grad_dtype="f16", grad_scale=1.0 / (1024 * world))
+        kw = dict(base_lr=32.0, grad_dtype="f16", grad_scale=1.0 / (1024 * world), shard_policy=policy,
+                  group_bytes=1 << 20)
         h = PK.Lars([(t.numel, t.kind) for t in lay], device=-1, nranks=world, **kw)
         hashes = [None] * world
         dist.all_gather_object(hashes, h.layout_hash())
@@ -46,15 +47,30 @@ def _worker(rank, world, port, errors):
         w, m = G.weights(lay), G.momentum(lay, 1e-3)
         hp = O.HParams(base_lr=32.0, grad_scale=kw["grad_scale"])
         ref = O.step(kinds, hp, 700, w, [G.grads(lay, q, 5, "f16") for q in range(world)], m)
-        b, e = h.shard_range(rank)
-        shard = np.zeros(e - b)
-        for l, t in enumerate(lay):
-            lo, hi = max(h.offsets[l], b), min(h.offsets[l] + t.numel, e)
-            if hi > lo:
-                shard[lo - b:hi - b] = ref.w[l][lo - h.offsets[l]:hi - h.offsets[l]]
-        parts = [torch.zeros(e - b, dtype=torch.float64) for _ in range(world)]
-        dist.all_gather(parts, torch.from_numpy(shard))
-        full = torch.cat(parts).numpy()
+        if policy == "groups":  # static groups: slice `rank` of every group, the same groups on every rank
+            groups = h.groups()
+            gs = [None] * world
+            dist.all_gather_object(gs, groups)
+            assert all(x == groups for x in gs) and len(groups) > 1
+            ranges = [(g["begin"] + rank * (g["len"] // world), g["begin"] + (rank + 1) * (g["len"] // world))
+                      for g in groups]
+        else:
+            ranges = [h.shard_range(rank)]
+        mine = np.zeros(h.padded_numel)
+        for b, e in ranges:
+            for l, t in enumerate(lay):
+                lo, hi = max(h.offsets[l], b), min(h.offsets[l] + t.numel, e)
+                if hi > lo:
+                    mine[lo:hi] = ref.w[l][lo - h.offsets[l]:hi - h.offsets[l]]
+        parts = [torch.zeros(h.padded_numel, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(mine))
+        owned = np.zeros(h.padded_numel, np.int64)  # every element owned by exactly one rank
+        full = np.zeros(h.padded_numel)
+        for r in range(world):
+            nz = parts[r].numpy() != 0
+            owned += nz
+            full += parts[r].numpy()
+        assert owned.max() <= 1
         for l in range(len(lay)):
             got = full[h.offsets[l]:h.offsets[l] + lay[l].numel]
             assert np.array_equal(got, ref.w[l]), f"tensor {l} not reassembled exactly"
@@ -70,13 +86,14 @@ def _worker(rank, world, port, errors):
         errors.put(f"rank {rank}: {ex}\n{traceback.format_exc()}")
 
 
-def test_dp_plan_and_sharded_update_world2_gloo():
+@pytest.mark.parametrize("policy", ["contiguous", "groups"])
+def test_dp_plan_and_sharded_update_world2_gloo(policy):
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     errors = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, errors)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, errors, policy)) for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:
