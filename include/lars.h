@@ -246,11 +246,15 @@ lars_status_t dp_group_ready(lars_handle_t h, const void* g, int32_t group, void
 
 /* Overlap trace (instrumentation for benchmarks and the schedule checker): lars_group_trace_enable(h, 1)
  * records timing events around every group's reduce-scatter from the next step on. lars_group_trace_read
- * synchronizes and returns, for the LAST step, milliseconds relative to group 0's ready event:
- * ready[k] (dp_group_ready or, for groups issued by the step itself, the step call), rs_start[k], rs_end[k]
- * (n = ngroups entries each) and *applied (the step's end on the caller's stream). Arrays may be NULL. */
+ * synchronizes and returns, for the LAST step, milliseconds relative to `ref_event` (a cudaEvent_t created
+ * with timing and recorded by the caller, passed as void*; NULL = group 0's ready event): ready[k]
+ * (dp_group_ready or, for groups issued by the step itself, the step call), rs_start[k], rs_end[k]
+ * (n = ngroups entries each) and *applied (the step's end on the caller's stream). Arrays may be NULL.
+ * The overlapped reduce-scatters use a split communicator limited to LARS_GROUP_MAX_CTAS CTAs (env,
+ * default 4; 0 = the main communicator) so they take few SMs from the backward kernels they overlap. */
 lars_status_t lars_group_trace_enable(lars_handle_t h, int32_t enable);
-lars_status_t lars_group_trace_read(lars_handle_t h, double* ready, double* rs_start, double* rs_end, double* applied);
+lars_status_t lars_group_trace_read(lars_handle_t h, void* ref_event, double* ready, double* rs_start, double* rs_end,
+                                    double* applied);
 
 /* dp_allreduce_lars_step with the iteration in device memory (see lars_step_dev_iter). */
 lars_status_t dp_allreduce_lars_step_dev_iter(lars_handle_t h, float* w, const void* g, float* m, int64_t* iter_dev,

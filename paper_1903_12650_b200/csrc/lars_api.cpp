@@ -194,6 +194,7 @@ struct lars_ctx {
   // caller reports it (dp_group_ready); the step issues the rest. Events: ready/rs_start/rs_end per group.
   int32_t next_group = 0;
   const void* group_g = nullptr;
+  ncclComm_t gcomm = nullptr;    // communicator of the overlapped group reduce-scatters (fewer CTAs)
   std::vector<cudaEvent_t> gev;  // [3*G + 2]: ready[k], rs0[k], rs1[k], then rs_all_done, applied
   bool gtrace = false, gtrace_valid = false;
 };
@@ -616,6 +617,17 @@ lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, cons
   if (cudaMalloc(&h->gred, red_elems * dtype_size(h->hp.grad_dtype)) != cudaSuccess) return LARS_ERR_OOM;
   CUDA_OR(cudaMemset(h->gred, 0, red_elems * dtype_size(h->hp.grad_dtype)));
   if (h->plan.policy == LARS_SHARD_GROUPS) {
+    // The group reduce-scatters run while the caller's backward kernels occupy the SMs: a split
+    // communicator with at most LARS_GROUP_MAX_CTAS CTAs per collective (default 4) keeps their footprint
+    // small (a collective waiting for a late peer spins on the SMs it holds). 0 = the main communicator.
+    const char* mc = getenv("LARS_GROUP_MAX_CTAS");
+    const int max_ctas = mc ? atoi(mc) : 4;
+    if (max_ctas > 0) {
+      ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+      cfg.minCTAs = 1;
+      cfg.maxCTAs = max_ctas;
+      NCCL_OR(ncclCommSplit(h->comm, 0, rank, &h->gcomm, &cfg));
+    }
     CUDA_OR(cudaStreamCreateWithFlags(&h->cs, cudaStreamNonBlocking));
     h->gev.assign(3 * h->plan.groups.size() + 2, nullptr);
     for (auto& e : h->gev) CUDA_OR(cudaEventCreate(&e));  // timing events (also used for ordering)
@@ -706,7 +718,7 @@ static lars_status_t issue_group(lars_handle_t h, const void* g, int32_t k, cuda
   CUDA_OR(cudaStreamWaitEvent(h->cs, h->gev[k], 0));
   if (h->gtrace) CUDA_OR(cudaEventRecord(h->gev[ng + k], h->cs));
   NCCL_OR(ncclReduceScatter((const char*)g + G.begin * esz, (char*)h->gred + (G.begin + h->rank * c) * esz,
-                            (size_t)c, nccl_type(dt), ncclSum, h->comm, h->cs));
+                            (size_t)c, nccl_type(dt), ncclSum, h->gcomm ? h->gcomm : h->comm, h->cs));
   if (h->gtrace) CUDA_OR(cudaEventRecord(h->gev[2 * ng + k], h->cs));
   return LARS_OK;
 }
@@ -773,7 +785,8 @@ lars_status_t lars_group_trace_enable(lars_handle_t h, int32_t enable) {
   return LARS_OK;
 }
 
-lars_status_t lars_group_trace_read(lars_handle_t h, double* ready, double* rs_start, double* rs_end, double* applied) {
+lars_status_t lars_group_trace_read(lars_handle_t h, void* ref_event, double* ready, double* rs_start, double* rs_end,
+                                    double* applied) {
   if (!h) return LARS_ERR_INVALID_ARG;
   if (!h->gtrace_valid) return LARS_ERR_NO_COMM;
   DeviceGuard dg(h->device);
@@ -781,7 +794,7 @@ lars_status_t lars_group_trace_read(lars_handle_t h, double* ready, double* rs_s
   CUDA_OR(cudaEventSynchronize(h->gev[3 * ng + 1]));
   auto rel = [&](cudaEvent_t e, double* out) -> lars_status_t {
     float ms = 0.f;
-    CUDA_OR(cudaEventElapsedTime(&ms, h->gev[0], e));
+    CUDA_OR(cudaEventElapsedTime(&ms, ref_event ? (cudaEvent_t)ref_event : h->gev[0], e));
     *out = ms;
     return LARS_OK;
   };
@@ -1033,6 +1046,7 @@ lars_status_t lars_destroy(lars_handle_t h) {
       for (auto e : h->gev)
         if (e) cudaEventDestroy(e);
       if (h->cs) cudaStreamDestroy(h->cs);
+      if (h->gcomm) ncclCommDestroy(h->gcomm);
       ncclCommDestroy(h->comm);
     }
     cudaFree(h->lr_d);

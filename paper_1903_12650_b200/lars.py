@@ -91,7 +91,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                   POINTER(c_int32)]),
         "dp_group_ready": (c_int32, [h, c_void_p, c_int32, c_void_p]),
         "lars_group_trace_enable": (c_int32, [h, c_int32]),
-        "lars_group_trace_read": (c_int32, [h, POINTER(c_double), POINTER(c_double), POINTER(c_double),
+        "lars_group_trace_read": (c_int32, [h, c_void_p, POINTER(c_double), POINTER(c_double), POINTER(c_double),
                                             POINTER(c_double)]),
         "lars_last_norms": (c_int32, [h, POINTER(c_double), POINTER(c_double), POINTER(c_double),
                                       POINTER(c_double)]),
@@ -300,11 +300,13 @@ class Lars:
     def group_trace_enable(self, on: bool = True) -> None:
         _check(self._lib.lars_group_trace_enable(self._h, 1 if on else 0), "lars_group_trace_enable")
 
-    def group_trace_read(self) -> dict:
-        """Last step, ms relative to group 0's ready event: ready/rs_start/rs_end per group, applied."""
+    def group_trace_read(self, ref_event=None) -> dict:
+        """Last step, ms relative to ref_event (a recorded torch.cuda.Event with timing; None = group 0's
+        ready event): ready/rs_start/rs_end per group, applied."""
         G = len(self.groups())
         r, a, b, ap = (c_double * G)(), (c_double * G)(), (c_double * G)(), c_double()
-        _check(self._lib.lars_group_trace_read(self._h, r, a, b, byref(ap)), "lars_group_trace_read")
+        ev = ref_event.cuda_event if ref_event is not None else None
+        _check(self._lib.lars_group_trace_read(self._h, ev, r, a, b, byref(ap)), "lars_group_trace_read")
         return {"ready": list(r), "rs_start": list(a), "rs_end": list(b), "applied": ap.value}
 
     def dp_allreduce_lars_step_host_grad(self, w, g_host, m, it: int, stream=None) -> None:

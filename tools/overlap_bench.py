@@ -2,12 +2,11 @@
 """Overlap of the gradient combine with backward via static groups (§III-C-2; SURVEY
 NEXT-f2), measured on B200 under torchrun (one process per GPU, NCCL).
 
-A synthetic backward pass produces the ResNet-50 gradients in backward order (last tensor first):
-  * --mode gemm (default): every conv / fc weight gradient is a real bf16 tensor-core GEMM of the layer's
-    backward shapes at the paper's per-GPU batch (81,920 / 2,048 = 40 images, 224 px): wgrad
-    dY^T [Cout x B*HW] . X [B*HW x Cin*k*k] written (as fp16) into the layer's slot of g, plus the dgrad
-    GEMM dY [B*HW x Cout] . W [Cout x Cin*k*k] whose output is discarded. BN/bias gradients are copies.
-  * --mode sleep: a 1-thread device spin per layer (SMs left free) + a copy.
+A synthetic backward pass produces the ResNet-50 gradients in backward order (last tensor first): every
+conv / fc weight gradient is a real bf16 tensor-core GEMM of the layer's backward shapes at the paper's
+per-GPU batch (81,920 / 2,048 = 40 images, 224 px): wgrad dY^T [Cout x B*HW] . X [B*HW x Cin*k*k] written
+(as fp16) into the layer's slot of g, plus the dgrad GEMM dY [B*HW x Cout] . W [Cout x Cin*k*k] whose output
+is discarded. BN/bias gradients are copies.
 Per configuration: (1) backward alone; (2) backward, then the whole dp step (no overlap): the NCCL path with
 contiguous shards and the fused NVLink path; (3) static groups at several thresholds, each group reported with
 dp_group_ready as soon as backward has written its last member. `exposed_ms` = iteration time - backward
@@ -50,10 +49,10 @@ def main():
 
     ap = argparse.ArgumentParser()
     ap.add_argument("--batch", type=int, default=40)
-    ap.add_argument("--mode", choices=("gemm", "sleep"), default="gemm")
     ap.add_argument("--thresholds", default="262144,1048576,4194304,16777216,67108864")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--max-ctas", default="4", help="LARS_GROUP_MAX_CTAS values to sweep (0 = main comm)")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     rank, P = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -83,24 +82,20 @@ def main():
     flops = sum(2 * 2 * M * N * K for (M, N, K) in (w for w in work if w))
     s = torch.cuda.current_stream()
 
-    def backward(h, g, gsrc, offsets, groups, report, done_ev=None, ready0_ev=None):
+    def backward(h, g, gsrc, offsets, groups, report, done_ev=None):
         gi = 0
         for l in range(L - 1, -1, -1):
             o, n = offsets[l], lay[l].numel
-            if work[l] is not None and a.mode == "gemm":
+            if work[l] is not None:
                 M, N, K = work[l]
                 dy, x = DY[:M * N].view(M, N), X[:M * K].view(M, K)
                 torch.mm(dy, W[:N * K].view(N, K), out=DX[:M * K].view(M, K))  # dgrad (discarded)
                 g[o:o + n].view(N, K).copy_(torch.mm(dy.t(), x))             # wgrad -> g (fp16)
             else:
-                if a.mode == "sleep":
-                    torch.cuda._sleep(20000 if work[l] is not None else 1000)
                 g[o:o + n].copy_(gsrc[o:o + n])
             if done_ev is not None:
                 done_ev[l].record(s)
             if report and groups is not None and l == groups[gi]["first"]:
-                if gi == 0 and ready0_ev is not None:
-                    ready0_ev.record(s)
                 h.dp_group_ready(g, gi)
                 gi += 1
 
@@ -140,10 +135,11 @@ def main():
             done = [torch.cuda.Event(enable_timing=True) for _ in range(L)]
             r0 = torch.cuda.Event(enable_timing=True)
             dist.barrier()
-            backward(h, g, gsrc, h.offsets, groups, True, done, r0)
+            r0.record(s)
+            backward(h, g, gsrc, h.offsets, groups, True, done)
             h.dp_allreduce_lars_step(w, g, m, 700)
             torch.cuda.synchronize()
-            tr = h.group_trace_read()
+            tr = h.group_trace_read(r0)
             bwd = {l: r0.elapsed_time(done[l]) for l in range(L)}
             bad = validate_trace(groups, bwd, tr, L, h.padded_numel)
             res.update(groups=len(groups), trace_ok=not bad, violations=bad[:3],
@@ -164,13 +160,16 @@ def main():
         r = run(label, **kw)
         r["exposed_ms"] = round(r["ms"] - bwd_ms, 4)
         out.append(r)
-    for thr in [int(x) for x in a.thresholds.split(",")]:
-        r = run(f"static groups {thr / 2**20:g} MiB, dp_group_ready during backward", policy="groups", thr=thr,
-                overlap=True)
-        r["exposed_ms"] = round(r["ms"] - bwd_ms, 4)
-        out.append(r)
+    for mc in [int(x) for x in a.max_ctas.split(",")]:
+        os.environ["LARS_GROUP_MAX_CTAS"] = str(mc)
+        for thr in [int(x) for x in a.thresholds.split(",")]:
+            r = run(f"static groups {thr / 2**20:g} MiB, max {mc} NCCL CTAs, dp_group_ready during backward",
+                    policy="groups", thr=thr, overlap=True)
+            r["exposed_ms"] = round(r["ms"] - bwd_ms, 4)
+            r["group_bytes"], r["max_ctas"] = thr, mc
+            out.append(r)
     if rank == 0:
-        head = {"P": P, "mode": a.mode, "batch_per_gpu": a.batch, "layout": "resnet50 (fp16 g)",
+        head = {"P": P, "backward": "bf16 GEMMs (dgrad + wgrad per conv/fc)", "batch_per_gpu": a.batch, "layout": "resnet50 (fp16 g)",
                 "backward_gemm_tflop": round(flops / 1e12, 4), "steps": a.steps}
         print(json.dumps(head), flush=True)
         for r in out:
