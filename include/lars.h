@@ -251,7 +251,7 @@ lars_status_t dp_group_ready(lars_handle_t h, const void* g, int32_t group, void
  * (dp_group_ready or, for groups issued by the step itself, the step call), rs_start[k], rs_end[k]
  * (n = ngroups entries each) and *applied (the step's end on the caller's stream). Arrays may be NULL.
  * The overlapped reduce-scatters use a split communicator limited to LARS_GROUP_MAX_CTAS CTAs (env,
- * default 4; 0 = the main communicator) so they take few SMs from the backward kernels they overlap. */
+ * default 8; 0 = the main communicator) so they take few SMs from the backward kernels they overlap. */
 lars_status_t lars_group_trace_enable(lars_handle_t h, int32_t enable);
 lars_status_t lars_group_trace_read(lars_handle_t h, void* ref_event, double* ready, double* rs_start, double* rs_end,
                                     double* applied);

@@ -618,10 +618,10 @@ lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, cons
   CUDA_OR(cudaMemset(h->gred, 0, red_elems * dtype_size(h->hp.grad_dtype)));
   if (h->plan.policy == LARS_SHARD_GROUPS) {
     // The group reduce-scatters run while the caller's backward kernels occupy the SMs: a split
-    // communicator with at most LARS_GROUP_MAX_CTAS CTAs per collective (default 4) keeps their footprint
+    // communicator with at most LARS_GROUP_MAX_CTAS CTAs per collective (default 8) keeps their footprint
     // small (a collective waiting for a late peer spins on the SMs it holds). 0 = the main communicator.
     const char* mc = getenv("LARS_GROUP_MAX_CTAS");
-    const int max_ctas = mc ? atoi(mc) : 4;
+    const int max_ctas = mc ? atoi(mc) : 8;
     if (max_ctas > 0) {
       ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
       cfg.minCTAs = 1;
