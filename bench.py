@@ -264,7 +264,6 @@ def run_ours(args):
     hbm = hbm or 6650.0
     shard_elems = sum(t.numel for t, o in zip(lay, h.tensor_owner()) if o == rank)
     upd_bytes = (4 + gbytes + 4 + 4 + 4) * shard_elems          # read w, g, m; write w, m
-    norm_bytes = (4 + gbytes) * shard_elems                      # read w, g
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
@@ -292,6 +291,7 @@ def run_ours(args):
                 "bus_bytes_per_step": int(bus), "peak_source": "measured peer copy per direction, B200_PROFILING.md",
                 "step_frac_of_bus_roofline": round(bus / NVLINK_PEER_GBS / 1e9 / (ms_step * 1e-3), 4)}
     step_alg = (upd_bytes) / (ms_step * 1e-3) / 1e9
+    two_pass = upd_bytes + (gbytes if carry else 4 + gbytes) * shard_elems
     out = {
         "metric": METRIC, "value": round(value, 1), "unit": "params/s", "n_gpus": P, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True, "scaling": "weak",
@@ -308,11 +308,15 @@ def run_ours(args):
         "roofline": roof,
         "roofline_step": {"bound": "hbm", "achieved": round(step_alg, 1), "peak": hbm, "unit": "GB/s",
                           "frac": round(step_alg / hbm, 4),
-                          "note": "algorithmic update bytes (w,g,m read; w,m write) / whole step time"},
+                          "note": "algorithmic update bytes (w,g,m read; w,m write) / whole step time",
+                          # the whole-step skip on a non-finite norm (reading #13) needs every norm before any
+                          # update, so g is streamed twice (norm pass, update pass; w too without carry)
+                          "two_pass_bytes": int(two_pass),
+                          "two_pass_frac": round(two_pass / (ms_step * 1e-3) / 1e9 / hbm, 4)},
         "e2e": {"value": round(units / (ms_e2e * 1e-3), 1), "unit": "params/s", "ms_per_step": round(ms_e2e, 4),
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "clocks": clk,
-        "gpu_launches": (3 if fused else 2 if P == 1 else 3) * args.steps,
+        "gpu_launches": (2 if fused else 2 if P == 1 else 3) * args.steps,
         "nccl_launches": (3 * args.steps) if (P > 1 and not fused) else 0,
     }
     if P == 1 and rank == 0 and not args.no_cpu_baseline:

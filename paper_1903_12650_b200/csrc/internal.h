@@ -22,6 +22,9 @@ constexpr int kThreads = 256;           // threads per CTA of K1 / K2
 #ifndef LARS_NORM_UNROLL
 #define LARS_NORM_UNROLL 2
 #endif
+#ifndef LARS_K1_KEEP_PCT  // carry mode: share of each tile's gradient K1 loads with L2::evict_last
+#define LARS_K1_KEEP_PCT 50
+#endif
 #ifndef LARS_NORM_UNROLL_G
 #define LARS_NORM_UNROLL_G 4
 #endif
@@ -54,6 +57,19 @@ struct Seg {
   int32_t tensor;  // local tensor index within the work list
 };
 static_assert(sizeof(Seg) == 16, "Seg is uploaded as-is");
+
+// Everything the per-segment finish of K1 needs, packed so one 32-byte load (prefetched during the chunk
+// stream) replaces a chain of dependent metadata loads.
+struct SegInfo {
+  int32_t a, b;        // chunk range [a, b) of the segment (absolute chunk ids)
+  int32_t tensor;      // local tensor id
+  int32_t nseg;        // segments of that tensor
+  int32_t split;       // global split slot or -1
+  int32_t lars;        // 1: weight kind (trust ratio + decay)
+  int32_t tseg_begin;  // first segment of the tensor
+  int32_t pad;
+};
+static_assert(sizeof(SegInfo) == 32, "SegInfo is uploaded as-is");
 
 // A work list: the tensors one launch of K1/K2 covers (all tensors for lars_step, the rank's
 // shard for the DP step), cut into ntiles tiles of (nearly) equal element count. Tile t covers
@@ -108,6 +124,7 @@ WorkList make_worklist(const Plan& plan, int32_t rank, int32_t ntiles_target, in
 
 // ---- kernel launchers (kernels.cu) ----
 struct DevWork {
+  const SegInfo* seginfo;
   const Seg* segs;
   const int32_t* tile_seg;
   const Seg* chunks;

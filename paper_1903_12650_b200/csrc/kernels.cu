@@ -177,6 +177,10 @@ struct LocalGrad {
   const void* g;
   int64_t shift;
   __device__ __forceinline__ F8 load8(int64_t e) const { return Grad<DT>::load8_keep(g, e - shift); }
+  // keep = false: the chunk is one K2 reads late (after L2 has turned over): do not displace kept lines
+  __device__ __forceinline__ F8 load8(int64_t e, bool keep) const {
+    return keep ? Grad<DT>::load8_keep(g, e - shift) : Grad<DT>::load8(g, e - shift);
+  }
   __device__ __forceinline__ float load1(int64_t e) const { return Grad<DT>::load1(g, e - shift); }
 };
 
@@ -214,6 +218,7 @@ struct PeerSumGrad {
     st8_noclobber(gred + (e - begin), acc);
     return acc;
   }
+  __device__ __forceinline__ F8 load8(int64_t e, bool) const { return load8(e); }
   __device__ __forceinline__ float load1(int64_t e) const {
     float acc = 0.f;
     for (int p = 0; p < nranks; ++p) acc += Grad<DT>::load1(gp[p], e);
@@ -221,6 +226,17 @@ struct PeerSumGrad {
     return acc;
   }
 };
+
+// Asynchronous global -> shared copies (LDGSTS): issued early, waited for with cp_async_wait_all().
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -268,12 +284,23 @@ __device__ __forceinline__ void warp_sum2(const double* xa, const double* xb, in
 
 // Per-layer finish from the layer's complete sums: ||w||, ||G|| = |s| sqrt(sum g^2), lambda, lr*lambda.
 // Returns true when a norm is non-finite (the step will be skipped).
-__device__ __forceinline__ bool finish_core(int32_t l, double sw, double sg, const DevWork& wk, const DevScratch& sc,
-                                            const Hyper& hy) {
+// lr(t) of this step and whether t is inside the schedule (read once per thread, early, off the critical path)
+struct StepLr {
+  double lr;
+  bool in_range;
+};
+__device__ __forceinline__ StepLr step_lr(const Hyper& hy) {
+  const int64_t t = hy.iter_dev ? *(volatile const int64_t*)hy.iter_dev : hy.iter;
+  const bool in_range = t >= 0 && t < hy.total_iters;  // host-given iterations are validated on the host
+  return StepLr{in_range ? hy.lr_table[t] : 0.0, in_range};
+}
+
+__device__ __forceinline__ bool finish_core(int32_t l, int32_t lars, double sw, double sg, const DevScratch& sc,
+                                            const Hyper& hy, const StepLr& slr) {
   const double wn = sqrt(sw);
   const double gn = fabs(hy.grad_scale) * sqrt(sg);
   double lam = 1.0, beta = 0.0;
-  if (wk.tlars[l]) {  // weight kind: trust ratio + decay (reading #1, #3); skip kinds keep 1, 0 (#4)
+  if (lars) {  // weight kind: trust ratio + decay (reading #1, #3); skip kinds keep 1, 0 (#4)
     beta = hy.weight_decay;
     const double den = gn + hy.weight_decay * wn + hy.eps;
     if (wn > 0.0 && den > 0.0) lam = hy.eta * wn / den;
@@ -281,22 +308,33 @@ __device__ __forceinline__ bool finish_core(int32_t l, double sw, double sg, con
   sc.w_norm[l] = wn;
   sc.g_norm[l] = gn;
   sc.lambda[l] = lam;
-  const int64_t t = hy.iter_dev ? *(volatile const int64_t*)hy.iter_dev : hy.iter;
-  const bool in_range = t >= 0 && t < hy.total_iters;  // host-given iterations are validated on the host
-  sc.coef[l] = in_range ? (float)(hy.lr_table[t] * lam) : 0.0f;
+  sc.coef[l] = slr.in_range ? (float)(slr.lr * lam) : 0.0f;
   sc.beta[l] = (float)beta;
-  return !(isfinite(wn) && isfinite(gn) && in_range);
+  return !(isfinite(wn) && isfinite(gn) && slr.in_range);
+}
+__device__ __forceinline__ bool finish_core(int32_t l, double sw, double sg, const DevWork& wk, const DevScratch& sc,
+                                            const Hyper& hy) {
+  return finish_core(l, wk.tlars[l], sw, sg, sc, hy, step_lr(hy));
 }
 
 template <class GL>
 __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, const DevScratch& sc, const Hyper& hy,
                                            const float* __restrict__ w, const GL& gl, double* sm_cw,
-                                           double* sm_cg, unsigned* sm_done, unsigned* sm_nonfinite, bool carried) {
+                                           double* sm_cg, unsigned* sm_done, unsigned* sm_nonfinite, bool carried,
+                                           const StepLr& slr) {
   constexpr int kWarps = kThreads / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int32_t s0 = wk.tile_seg[tile], s1 = wk.tile_seg[tile + 1];
+  // Copied into shared memory under the chunk stream (cp.async, no registers held): every warp's first
+  // segment finish record, and in carry mode the tile's carried chunk sums of w^2 (<= kMaxTileChunks ==
+  // kThreads, one per thread).
+  __shared__ __align__(16) SegInfo sm_si[kThreads / 32];
+  static_assert(kMaxTileChunks <= kThreads, "one carried chunk partial per thread");
   // Phase A: the warps of the CTA stream the tile's chunks independently (no block barrier per layer);
   // chunk partials stay in shared memory.
   const int32_t c0 = wk.tile_chunk[tile], c1 = wk.tile_chunk[tile + 1];
+  if (carried && tid < c1 - c0) cp_async8(sm_cw + tid, sc.cpart_wnext + c0 + tid);
+  if (lane < 2 && s0 + warp < s1) cp_async16((char*)(sm_si + warp) + 16 * lane, (const char*)(wk.seginfo + s0 + warp) + 16 * lane);
   // chunk descriptors are prefetched one iteration ahead (their load would otherwise add a round trip
   // in front of every chunk's data loads)
   Seg nxt = (c0 + warp < c1) ? wk.chunks[c0 + warp] : Seg{0, 0, 0};
@@ -310,10 +348,12 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
       double ag = 0.0, ag1 = 0.0;
       int32_t j = lane;
       constexpr int U = GL::kUnrollG;  // local source: 4 x 32 B in flight per lane
+      // K2 walks every tile's parts last-to-first: only the tail of each tile can still be in L2 then
+      const bool keep = (int64_t)(c - c0) * 100 >= (int64_t)(c1 - c0) * (100 - LARS_K1_KEEP_PCT);
       for (; j + (U - 1) * 32 < ng; j += U * 32) {
         F8 gv[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) gv[u] = gl.load8(gi + 8 * (j + 32 * u));
+        for (int u = 0; u < U; ++u) gv[u] = gl.load8(gi + 8 * (j + 32 * u), keep);
 #pragma unroll
         for (int u = 0; u < U; u += 2) {
           acc8(ag, gv[u]);
@@ -328,10 +368,7 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) ag += __shfl_xor_sync(0xffffffffu, ag, o);
-      if (lane == 0) {
-        sm_cw[c - c0] = __ldcg(sc.cpart_wnext + c);
-        sm_cg[c - c0] = ag;
-      }
+      if (lane == 0) sm_cg[c - c0] = ag;
       continue;
     }
     double aw = 0.0, ag = 0.0, aw1 = 0.0, ag1 = 0.0;
@@ -377,13 +414,15 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
       sm_cg[c - c0] = ag;
     }
   }
+  cp_async_wait_all();
   __syncthreads();  // every chunk partial of this tile is in shared memory
+  TRACE_MARK_AT(4, 0)
   // Phase B: one warp per segment sums its chunk partials (fixed order). A layer that lies inside this
   // tile is finished right here (no global traffic beyond its outputs); a layer spread over several
   // tiles publishes the segment partial and the warp that brings in its last segment finishes it.
-  const int32_t s0 = wk.tile_seg[tile], s1 = wk.tile_seg[tile + 1];
   for (int32_t s = s0 + warp; s < s1; s += kWarps) {
-    const int32_t a = wk.seg_chunk[s] - c0, b = wk.seg_chunk[s + 1] - c0;
+    const SegInfo si = (s == s0 + warp) ? sm_si[warp] : wk.seginfo[s];
+    const int32_t a = si.a - c0, b = si.b - c0;
     double tw = 0.0, tg = 0.0;
     for (int32_t i = a + lane; i < b; i += 32) {
       tw += sm_cw[i];
@@ -394,15 +433,15 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
       tw += __shfl_xor_sync(0xffffffffu, tw, o);
       tg += __shfl_xor_sync(0xffffffffu, tg, o);
     }
-    const int32_t l = wk.segs[s].tensor;
-    const int32_t nseg = wk.tseg_count[l];
-    const int32_t split = wk.tsplit[l];
+    const int32_t l = si.tensor;
+    const int32_t nseg = si.nseg;
+    const int32_t split = si.split;
     if (nseg == 1) {
       if (lane == 0) {
         if (split >= 0) {  // straddles ranks: publish this rank's share for the C3 allreduce
           sc.c3[1 + 2 * split] = tw;
           sc.c3[2 + 2 * split] = tg;
-        } else if (finish_core(l, tw, tg, wk, sc, hy)) {
+        } else if (finish_core(l, si.lars, tw, tg, sc, hy, slr)) {
           atomicOr(sm_nonfinite, 1u);
         }
         atomicAdd(sm_done, 1u);
@@ -419,7 +458,7 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
     prev = __shfl_sync(0xffffffffu, prev, 0);
     if (prev == (unsigned)nseg - 1u) {  // last segment of layer l: this warp finishes it
       __threadfence();
-      const int32_t sb = wk.tseg_begin[l];
+      const int32_t sb = si.tseg_begin;
       double sw = 0.0, sg = 0.0;
       for (int32_t i = sb + lane; i < sb + nseg; i += 32) {
         sw += __ldcg(sc.part_w + i);
@@ -435,7 +474,7 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
         if (split >= 0) {
           sc.c3[1 + 2 * split] = sw;
           sc.c3[2 + 2 * split] = sg;
-        } else if (finish_core(l, sw, sg, wk, sc, hy)) {
+        } else if (finish_core(l, si.lars, sw, sg, sc, hy, slr)) {
           atomicOr(sm_nonfinite, 1u);
         }
         atomicAdd(sm_done, 1u);
@@ -467,6 +506,7 @@ __device__ __forceinline__ bool norms_body(const DevWork& wk, const DevScratch& 
   __syncthreads();
   // carry mode: the previous K2 left sum(w_new^2) per chunk; valid until the host invalidates it
   const bool carried = CARRY && *(volatile const int32_t*)sc.wnext_valid != 0;
+  const StepLr slr = step_lr(hy);
   if (DYN) {  // tiles handed out by a ticket counter (faster CTAs take more tiles)
     __shared__ int32_t s_tile;
     if (threadIdx.x == 0) s_tile = take_ticket(sc.ticket + 0, wk.ntiles, gridDim.x);
@@ -476,7 +516,7 @@ __device__ __forceinline__ bool norms_body(const DevWork& wk, const DevScratch& 
       __syncthreads();  // s_tile read by all; shared chunk partials of the previous tile consumed
       int32_t next = 0;
       if (threadIdx.x == 0) next = take_ticket(sc.ticket + 0, wk.ntiles, gridDim.x);
-      norms_tile(tile, wk, sc, hy, w, gl, sm_cw, sm_cg, &sm_done, &sm_nonfinite, carried);
+      norms_tile(tile, wk, sc, hy, w, gl, sm_cw, sm_cg, &sm_done, &sm_nonfinite, carried, slr);
       __syncthreads();
       if (threadIdx.x == 0) s_tile = next;
       __syncthreads();
@@ -485,7 +525,7 @@ __device__ __forceinline__ bool norms_body(const DevWork& wk, const DevScratch& 
   } else {
     for (int32_t tile = blockIdx.x; tile < wk.ntiles; tile += gridDim.x) {
       __syncthreads();  // shared chunk partials of the previous tile fully consumed
-      norms_tile(tile, wk, sc, hy, w, gl, sm_cw, sm_cg, &sm_done, &sm_nonfinite, carried);
+      norms_tile(tile, wk, sc, hy, w, gl, sm_cw, sm_cg, &sm_done, &sm_nonfinite, carried, slr);
     }
   }
   __syncthreads();

@@ -63,6 +63,7 @@ lars_status_t upload(DevBufs& b, int sms, int32_t nsplit_total, bool dp) {
                ntl = wl.tile_seg.size(), nc = std::max<size_t>(wl.chunks.size(), 1);
   size_t bytes = 0;
   auto add = [&](size_t n, size_t sz) { bytes += (n * sz + 255) / 256 * 256; };
+  add(ns, sizeof(SegInfo));                                                             // segment finish info
   add(ns, sizeof(Seg)); add(ntl, 4); add(nt, 4); add(nt, 4); add(nt, 4);                // work list
   add(nc, sizeof(Seg)); add(ntl, 4); add(ns + 1, 4); add(nc, 8); add(nc, 8);            // chunks
   add(nc, 8); add(1, 4);                                                                // carried norms
@@ -73,6 +74,7 @@ lars_status_t upload(DevBufs& b, int sms, int32_t nsplit_total, bool dp) {
   if (cudaMalloc(&b.mem, bytes) != cudaSuccess) return LARS_ERR_OOM;
   if (cudaMemset(b.mem, 0, bytes) != cudaSuccess) return LARS_ERR_CUDA;
   char* p = (char*)b.mem;
+  SegInfo* seginfo = carve<SegInfo>(p, ns);
   Seg* segs = carve<Seg>(p, ns);
   int32_t* tile_seg = carve<int32_t>(p, ntl);
   int32_t* tsb = carve<int32_t>(p, nt);
@@ -105,6 +107,13 @@ lars_status_t upload(DevBufs& b, int sms, int32_t nsplit_total, bool dp) {
   b.sc.coef = carve<float>(p, nt);
   b.sc.beta = carve<float>(p, nt);
   auto cp = [](void* d, const void* s, size_t n) { return n == 0 || cudaMemcpy(d, s, n, cudaMemcpyHostToDevice) == cudaSuccess; };
+  std::vector<SegInfo> si(wl.segs.size());
+  for (size_t k = 0; k < wl.segs.size(); ++k) {
+    const int32_t l = wl.segs[k].tensor;
+    si[k] = SegInfo{wl.seg_chunk[k], wl.seg_chunk[k + 1], l, wl.tseg_count[l], wl.tsplit[l], wl.tlars[l],
+                    wl.tseg_begin[l], 0};
+  }
+  if (!cp(seginfo, si.data(), si.size() * sizeof(SegInfo))) return LARS_ERR_CUDA;
   if (!(cp(segs, wl.segs.data(), wl.segs.size() * sizeof(Seg)) && cp(tile_seg, wl.tile_seg.data(), ntl * 4) &&
         cp(tsb, wl.tseg_begin.data(), wl.tseg_begin.size() * 4) &&
         cp(tsc, wl.tseg_count.data(), wl.tseg_count.size() * 4) && cp(tl, wl.tlars.data(), wl.tlars.size() * 4) &&
@@ -112,7 +121,7 @@ lars_status_t upload(DevBufs& b, int sms, int32_t nsplit_total, bool dp) {
         cp(seg_chunk, wl.seg_chunk.data(), wl.seg_chunk.size() * 4) &&
         cp(tsplit, wl.tsplit.data(), wl.tsplit.size() * 4) && cp(split_locals, locals.data(), locals.size() * 4)))
     return LARS_ERR_CUDA;
-  b.dw = DevWork{segs, tile_seg, chunks, tile_chunk, seg_chunk, tsb, tsc, tl, tsplit, split_locals,
+  b.dw = DevWork{seginfo, segs, tile_seg, chunks, tile_chunk, seg_chunk, tsb, tsc, tl, tsplit, split_locals,
                  (int32_t)locals.size(), dp ? nsplit_total : 0, wl.ntiles(), (int32_t)wl.tensors.size(),
                  std::min<int32_t>(wl.ntiles(), sms * kCtasPerSm)};
   (void)sms;

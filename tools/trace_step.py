@@ -27,16 +27,30 @@ def main():
     w = torch.from_numpy(G.pack(G.weights(lay), h.offsets, h.padded_numel)).to(dev)
     g = torch.from_numpy(G.pack(G.grads(lay, 0, 0, dtype), h.offsets, h.padded_numel)).to(dev)
     m = torch.from_numpy(G.pack(G.momentum(lay, 1e-3), h.offsets, h.padded_numel)).to(dev)
-    buf = torch.zeros(2 * 4096 * 4, dtype=torch.int64, device=dev)
+    buf = torch.zeros(6 * 4096 * 4, dtype=torch.int64, device=dev)
     lib.lars_trace_arm.argtypes = [ctypes.c_void_p]
     for i in range(30):
         h.lars_step(w, g, m, 719 + i)
     torch.cuda.synchronize()
     assert lib.lars_trace_arm(buf.data_ptr()) == 0
-    for i in range(3):
+    spans = []
+    for i in range(12):  # per step: K1 span, K1->K2 gap, K2 span, K1 start -> K2 end
         h.lars_step(w, g, m, 800 + i)
         torch.cuda.synchronize()
-    tr = buf.view(2, 4096, 4).cpu().numpy()
+        x = buf.view(6, 4096, 4).cpu().numpy()
+        n1, n2 = int(x[0, 0, 3]), int(x[1, 0, 3])
+        a0, a1 = x[0, :n1, 0].min(), x[0, :n1, 1].max()
+        b0, b1 = x[1, :n2, 0].min(), x[1, :n2, 1].max()
+        spans.append(((a1 - a0) / 1e3, (b0 - a1) / 1e3, (b1 - b0) / 1e3, (b1 - a0) / 1e3))
+    med = np.median(np.array(spans[2:]), axis=0)
+    print(f"median over 10 steps: K1 {med[0]:.2f} us, gap {med[1]:.2f}, K2 {med[2]:.2f}, K1+K2 {med[3]:.2f}")
+    tr = buf.view(6, 4096, 4).cpu().numpy()
+    n1 = int(tr[0, 0, 3])
+    t0k1 = tr[0, :n1, 0].min()
+    pa = (tr[4, :n1, 0] - t0k1) / 1e3
+    print(f"K1 phase A (chunk streaming) done: min/p50/max = {pa.min():.1f}/{np.median(pa):.1f}/{pa.max():.1f} us")
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    np.save(os.path.join(ROOT, "gpurun_out", "trace_step.npy"), tr)
     for k, name in enumerate(["K1 norms", "K2 update"]):
         n = int(tr[k, 0, 3])
         t = tr[k, :n]
