@@ -30,7 +30,13 @@ constexpr int kThreads = 256;           // threads per CTA of K1 / K2
 #endif
 constexpr int kCtasPerSm = LARS_NORM_CTAS_PER_SM;      // K1 resident CTAs per SM (one static tile each)
 // fused F1 CTAs per SM: 2 ranks fit 64 registers (4 CTAs/SM); 3-8 ranks' loads per vector need 128 (2/SM)
-constexpr int dp_norm_ctas_per_sm(int nranks) { return nranks <= 2 ? 4 : 2; }
+#ifndef LARS_DP_UNROLL_G2  // F1 at P <= 2, carried norms: gradient groups per lane per iteration
+#define LARS_DP_UNROLL_G2 2
+#endif
+#ifndef LARS_DP_CTAS2  // F1 CTAs per SM at P <= 2
+#define LARS_DP_CTAS2 4
+#endif
+constexpr int dp_norm_ctas_per_sm(int nranks) { return nranks <= 2 ? LARS_DP_CTAS2 : 2; }
 #ifndef LARS_DP_TILES_PER_CTA
 #define LARS_DP_TILES_PER_CTA 1
 #endif

@@ -195,7 +195,7 @@ struct PeerSumGrad {
   float* gred;                // local fp32 reduced shard: element e at gred[e - begin]
   int64_t begin;
   static constexpr int kUnroll = 1;                 // (w, g) groups per lane per iteration (register budget)
-  static constexpr int kUnrollG = NP <= 2 ? 2 : 1;  // g-only groups per lane per iteration (carried norms)
+  static constexpr int kUnrollG = NP <= 2 ? LARS_DP_UNROLL_G2 : 1;  // g-only groups per lane per iteration (carry)
   static constexpr int kBatch = NP < 4 ? NP : 4;   // peer loads issued back to back before decoding
   __device__ __forceinline__ F8 load8(int64_t e) const {
     F8 acc;

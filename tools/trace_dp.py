@@ -23,7 +23,7 @@ def main():
     torch.cuda.set_device(rank)
     dev = torch.device("cuda", rank)
     dist.init_process_group("nccl", device_id=dev)
-    lib = PK.load_library(os.path.join(ROOT, "build", "liblars_trace.so"))
+    lib = PK.load_library(os.path.join(ROOT, "build", f"liblars_trace{os.environ.get('TRACE_TAG', '')}.so"))
     lay = LY.resnet50()
     h = PK.Lars([(t.numel, t.kind) for t in lay], device=rank, grad_dtype="f16", nranks=P, base_lr=32.0,
                 grad_scale=1 / (1024 * P), flags=1)
@@ -39,9 +39,18 @@ def main():
     torch.cuda.synchronize()
     assert lib.lars_trace_arm(buf.data_ptr()) == 0
     dist.barrier()
-    for i in range(3):
+    spans = []
+    for i in range(12):
+        dist.barrier()
         h.dp_allreduce_lars_step(w, g, m, 740 + i)
         torch.cuda.synchronize()
+        x = buf.view(6, 4096, 4).cpu().numpy()
+        a, b = x[2], x[3]
+        n1_, n2_ = int(a[0, 3]), int(b[0, 3])
+        s0 = a[:n1_, 0].min()
+        spans.append(((x[5][:n1_, 2].max() - s0) / 1e3, (a[:n1_, 1].max() - s0) / 1e3, (b[:n2_, 1].max() - s0) / 1e3))
+    med = np.median(np.array(spans[2:]), axis=0)
+    print(f"rank {rank} median of 10: barrier past {med[0]:.1f} us, F1 end {med[1]:.1f}, F2 end {med[2]:.1f}", flush=True)
     tr = buf.view(6, 4096, 4).cpu().numpy()
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     np.save(os.path.join(ROOT, "gpurun_out", f"trace_dp_p{P}_r{rank}.npy"), tr)
