@@ -32,7 +32,7 @@ def main():
     w.copy_(torch.from_numpy(G.pack(G.weights(lay), h.offsets, h.padded_numel)))
     g.copy_(torch.from_numpy(G.pack(G.grads(lay, rank, 0, "f16"), h.offsets, h.padded_numel)))
     m = torch.from_numpy(G.pack(G.momentum(lay, 1e-3), h.offsets, h.padded_numel)).to(dev)
-    buf = torch.zeros(6 * 4096 * 4, dtype=torch.int64, device=dev)
+    buf = torch.zeros(8 * 4096 * 4, dtype=torch.int64, device=dev)
     lib.lars_trace_arm.argtypes = [ctypes.c_void_p]
     for i in range(20):
         h.dp_allreduce_lars_step(w, g, m, 719 + i)
@@ -44,14 +44,16 @@ def main():
         dist.barrier()
         h.dp_allreduce_lars_step(w, g, m, 740 + i)
         torch.cuda.synchronize()
-        x = buf.view(6, 4096, 4).cpu().numpy()
+        x = buf.view(8, 4096, 4).cpu().numpy()
         a, b = x[2], x[3]
         n1_, n2_ = int(a[0, 3]), int(b[0, 3])
-        s0 = a[:n1_, 0].min()
+        f0 = x[6]
+        n0_ = int(f0[0, 3])
+        s0 = min(a[:n1_, 0].min(), f0[:n0_, 0].min()) if n0_ else a[:n1_, 0].min()
         spans.append(((x[5][:n1_, 2].max() - s0) / 1e3, (a[:n1_, 1].max() - s0) / 1e3, (b[:n2_, 1].max() - s0) / 1e3))
     med = np.median(np.array(spans[2:]), axis=0)
     print(f"rank {rank} median of 10: barrier past {med[0]:.1f} us, F1 end {med[1]:.1f}, F2 end {med[2]:.1f}", flush=True)
-    tr = buf.view(6, 4096, 4).cpu().numpy()
+    tr = buf.view(8, 4096, 4).cpu().numpy()
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     np.save(os.path.join(ROOT, "gpurun_out", f"trace_dp_p{P}_r{rank}.npy"), tr)
     f1, f2, mk = tr[2], tr[3], tr[5]
