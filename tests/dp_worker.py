@@ -214,6 +214,10 @@ def main():
              ("r50-f16", lay_r50, "f16", 719, {}),
              ("r50-int", lay_r50, "f16", 1439, dict(kind="integer")),
              ("r50-lpt-f16", lay_r50, "f16", 80, dict(shard_policy="lpt")),
+             # 3 layers, whole-layer shards: at P >= 4 a rank owns no layer (it still takes part in every
+             # collective and advances its iteration)
+             ("tiny-lpt-f16", LY.tiny(), "f16", 80, dict(shard_policy="lpt")),
+             ("fused-tiny-lpt-f16", LY.tiny(), "f16", 81, dict(shard_policy="lpt", fused=True)),
              ("r50-f16-buckets4", lay_r50, "f16", 81, dict(buckets=4)),
              ("random-bf16-buckets3", LY.random_layout(np.random.default_rng(18), 40), "bf16", 82, dict(buckets=3)),
              ("r50-int-buckets8-carry", lay_r50, "f16", 83, dict(kind="integer", buckets=8, flags=1)),
