@@ -630,72 +630,82 @@ struct McastWeights {
   }
 };
 
-template <int DT, bool CARRY, class WS = NoPeers>
+// One warp chunk of K2 (and F2): unscale + weight decay + momentum + update of <= kChunk elements, every new
+// weight also handed to `ws` (the other ranks' buffers on the fused path); carry mode also leaves the chunk's
+// sum(w_new^2) for the next step's K1.
+template <int DT, bool CARRY, typename WS = NoPeers>
+__device__ __forceinline__ void update_chunk(int32_t c, const DevWork& wk, const DevScratch& sc, const Hyper& hy,
+                                             float* __restrict__ w, const void* __restrict__ g, int64_t g_shift,
+                                             float* __restrict__ m, const WS& ws = WS()) {
+  const int lane = threadIdx.x & 31;
+  const float s = hy.grad_scale_f, mu = hy.mu;
+  const Seg ck = wk.chunks[c];
+  const float cf = sc.coef[ck.tensor], b = sc.beta[ck.tensor];
+  float* wp = w + ck.begin;
+  float* mp = m + ck.begin;
+  const int64_t gi = ck.begin - g_shift;
+  const int32_t ng = ck.len >> 3;
+  double aw = 0.0, aw1 = 0.0;  // CARRY: sum(w_new^2) of this chunk for the next step's K1
+  for (int32_t i = (ng << 3) + lane; i < ck.len; i += 32) {  // ragged tensor tail (< 8 elements)
+    const float wv = wp[i], mv = mp[i];
+    const float u = fmaf(b, wv, s * Grad<DT>::load1(g, gi + i));
+    const float v = hy.lr_at_apply ? fmaf(mu, mv, u) : fmaf(mu, mv, cf * u);
+    const float wn = hy.lr_at_apply ? fmaf(-cf, v, wv) : wv - v;
+    wp[i] = wn;
+    mp[i] = v;
+    ws.store1(ck.begin + i, wn);
+    if (CARRY) aw = fma((double)wn, (double)wn, aw);
+  }
+  int32_t j = ng - 1 - lane;
+  for (; j - 32 >= 0; j -= 64) {
+    const int32_t j1 = j - 32;
+    F8 w0 = ld8_rw(wp + 8 * j), w1 = ld8_rw(wp + 8 * j1);
+    const F8 g0 = Grad<DT>::load8(g, gi + 8 * j), g1 = Grad<DT>::load8(g, gi + 8 * j1);
+    F8 m0 = ld8_rw(mp + 8 * j), m1 = ld8_rw(mp + 8 * j1);
+    upd8(w0, m0, g0, s, cf, b, mu, hy.lr_at_apply);
+    upd8(w1, m1, g1, s, cf, b, mu, hy.lr_at_apply);
+    st8(wp + 8 * j, w0);
+    st8(mp + 8 * j, m0);
+    st8(wp + 8 * j1, w1);
+    st8(mp + 8 * j1, m1);
+    ws.store8(ck.begin + 8 * j, w0);
+    ws.store8(ck.begin + 8 * j1, w1);
+    if (CARRY) {
+      accw8(aw, w0);
+      accw8(aw1, w1);
+    }
+  }
+  if (j >= 0) {
+    F8 w0 = ld8_rw(wp + 8 * j), m0 = ld8_rw(mp + 8 * j);
+    const F8 g0 = Grad<DT>::load8(g, gi + 8 * j);
+    upd8(w0, m0, g0, s, cf, b, mu, hy.lr_at_apply);
+    st8(wp + 8 * j, w0);
+    st8(mp + 8 * j, m0);
+    ws.store8(ck.begin + 8 * j, w0);
+    if (CARRY) accw8(aw, w0);
+  }
+  if (CARRY) {
+    aw += aw1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) aw += __shfl_xor_sync(0xffffffffu, aw, o);
+    if (lane == 0) sc.cpart_wnext[c] = aw;
+  }
+}
+
+template <int DT, bool CARRY, typename WS = NoPeers>
 __device__ __forceinline__ void update_item(int32_t item, const DevWork& wk, const DevScratch& sc, const Hyper& hy,
                                             float* __restrict__ w, const void* __restrict__ g, int64_t g_shift,
                                             float* __restrict__ m, const WS& ws = WS()) {
   constexpr int kWarps = kThreads / 32;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const float s = hy.grad_scale_f, mu = hy.mu;
+  const int warp = threadIdx.x >> 5;
   // item -> (part q, tile): all tiles' last parts first (the bytes K1 read last, still in L2), then the
   // next-to-last parts, ...; inside a part the chunks run backwards.
   const int32_t q = kUpdateSplit - 1 - item / wk.ntiles, tile = item % wk.ntiles;
   const int32_t t0 = wk.tile_chunk[tile], tn = wk.tile_chunk[tile + 1] - t0;
   const int32_t c0 = t0 + (int32_t)((int64_t)tn * q / kUpdateSplit);
   const int32_t c1 = t0 + (int32_t)((int64_t)tn * (q + 1) / kUpdateSplit);
-  for (int32_t c = c1 - 1 - warp; c >= c0; c -= kWarps) {  // backwards: K1's most recent reads first
-    const Seg ck = wk.chunks[c];
-    const float cf = sc.coef[ck.tensor], b = sc.beta[ck.tensor];
-    float* wp = w + ck.begin;
-    float* mp = m + ck.begin;
-    const int64_t gi = ck.begin - g_shift;
-    const int32_t ng = ck.len >> 3;
-    double aw = 0.0, aw1 = 0.0;  // CARRY: sum(w_new^2) of this chunk for the next step's K1
-    for (int32_t i = (ng << 3) + lane; i < ck.len; i += 32) {  // ragged tensor tail (< 8 elements)
-      const float wv = wp[i], mv = mp[i];
-      const float u = fmaf(b, wv, s * Grad<DT>::load1(g, gi + i));
-      const float v = hy.lr_at_apply ? fmaf(mu, mv, u) : fmaf(mu, mv, cf * u);
-      const float wn = hy.lr_at_apply ? fmaf(-cf, v, wv) : wv - v;
-      wp[i] = wn;
-      mp[i] = v;
-      ws.store1(ck.begin + i, wn);
-      if (CARRY) aw = fma((double)wn, (double)wn, aw);
-    }
-    int32_t j = ng - 1 - lane;
-    for (; j - 32 >= 0; j -= 64) {
-      const int32_t j1 = j - 32;
-      F8 w0 = ld8_rw(wp + 8 * j), w1 = ld8_rw(wp + 8 * j1);
-      const F8 g0 = Grad<DT>::load8(g, gi + 8 * j), g1 = Grad<DT>::load8(g, gi + 8 * j1);
-      F8 m0 = ld8_rw(mp + 8 * j), m1 = ld8_rw(mp + 8 * j1);
-      upd8(w0, m0, g0, s, cf, b, mu, hy.lr_at_apply);
-      upd8(w1, m1, g1, s, cf, b, mu, hy.lr_at_apply);
-      st8(wp + 8 * j, w0);
-      st8(mp + 8 * j, m0);
-      st8(wp + 8 * j1, w1);
-      st8(mp + 8 * j1, m1);
-      ws.store8(ck.begin + 8 * j, w0);
-      ws.store8(ck.begin + 8 * j1, w1);
-      if (CARRY) {
-        accw8(aw, w0);
-        accw8(aw1, w1);
-      }
-    }
-    if (j >= 0) {
-      F8 w0 = ld8_rw(wp + 8 * j), m0 = ld8_rw(mp + 8 * j);
-      const F8 g0 = Grad<DT>::load8(g, gi + 8 * j);
-      upd8(w0, m0, g0, s, cf, b, mu, hy.lr_at_apply);
-      st8(wp + 8 * j, w0);
-      st8(mp + 8 * j, m0);
-      ws.store8(ck.begin + 8 * j, w0);
-      if (CARRY) accw8(aw, w0);
-    }
-    if (CARRY) {
-      aw += aw1;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) aw += __shfl_xor_sync(0xffffffffu, aw, o);
-      if (lane == 0) sc.cpart_wnext[c] = aw;
-    }
-  }
+  for (int32_t c = c1 - 1 - warp; c >= c0; c -= kWarps)  // backwards: K1's most recent reads first
+    update_chunk<DT, CARRY, WS>(c, wk, sc, hy, w, g, g_shift, m, ws);
 }
 
 // K2. Same persistent schedule as K1 (CTA b owns tiles b, b + grid, ...; identical grid and resources,
