@@ -236,6 +236,20 @@ def run_ours(args):
         h.invalidate_carried_norms()  # w was advanced by another handle
     if P > 1 and fused:
         alt["nccl_path_ms_per_step"] = time_loop(h.dp_allreduce_lars_step, w_n, g_n)
+        # the NCCL path's phases, with reduce-scatter / all-gather bus bandwidth (nccl-tests convention:
+        # busBW = (P-1)/P * bytes / t, bytes = the full buffer)
+        h.profile_enable(True)
+        barrier()
+        for i in range(nprof):
+            h.dp_allreduce_lars_step(w_n, g_n, m, (T0 + i) % T, stream)
+        nph, nn = h.profile_read()
+        h.profile_enable(False)
+        nph = {kk: max_over_ranks(v / max(1, nn)) for kk, v in nph.items()}
+        gb = h.padded_numel * (2 if dtype != "f32" else 4)
+        alt["nccl_path_phases_ms"] = {kk: round(v, 5) for kk, v in nph.items()}
+        alt["nccl_rs_busbw_GBps"] = round((P - 1) / P * gb / (nph["reduce_scatter"] * 1e-3) / 1e9, 1)
+        alt["nccl_ag_busbw_GBps"] = round((P - 1) / P * h.padded_numel * 4 / (nph["all_gather"] * 1e-3) / 1e9, 1)
+        alt["nccl_nvls_enable"] = os.environ.get("NCCL_NVLS_ENABLE", "default")
 
     # end to end through the public API with host gradients
     g_pin = torch.from_numpy(G.pack(g_host, h.offsets, h.padded_numel)).pin_memory()  # lands in g's buffer
@@ -281,7 +295,7 @@ def run_ours(args):
         bus = (P - 1) / P * (gbytes + 4) * h.padded_numel
         if fused:  # F1 (reduce+norms) + FX + F2 (update+gather): the transfers ARE these kernels
             coll_ms = ph["norms"] + ph["skip_allreduce"] + ph["update"]
-            kname = "fused NVLink path F1 reduce+norms, FX, F2 update+gather"
+            kname = "fused NVLink path: F1 reduce+norms, F2 update+gather"
         else:
             coll_ms = ph["reduce_scatter"] + ph["all_gather"]
             kname = "NCCL reduce-scatter + all-gather (C1+C2)"
@@ -306,13 +320,17 @@ def run_ours(args):
                          "no flush"},
         "phases_ms": {kk: round(v, 5) for kk, v in ph.items() if v > 0},
         "roofline": roof,
-        "roofline_step": {"bound": "hbm", "achieved": round(step_alg, 1), "peak": hbm, "unit": "GB/s",
-                          "frac": round(step_alg / hbm, 4),
-                          "note": "algorithmic update bytes (w,g,m read; w,m write) / whole step time",
-                          # the whole-step skip on a non-finite norm (reading #13) needs every norm before any
-                          # update, so g is streamed twice (norm pass, update pass; w too without carry)
-                          "two_pass_bytes": int(two_pass),
-                          "two_pass_frac": round(two_pass / (ms_step * 1e-3) / 1e9 / hbm, 4)},
+        "roofline_step": ({"bound": "hbm", "achieved": round(step_alg, 1), "peak": hbm, "unit": "GB/s",
+                           "frac": round(step_alg / hbm, 4),
+                           "note": "algorithmic update bytes (w,g,m read; w,m write) / whole step time",
+                           # the whole-step skip on a non-finite norm (reading #13) needs every norm before any
+                           # update, so g is streamed twice (norm pass, update pass; w too without carry)
+                           "two_pass_bytes": int(two_pass),
+                           "two_pass_frac": round(two_pass / (ms_step * 1e-3) / 1e9 / hbm, 4)} if P == 1 else
+                          {"bound": "nvlink", "achieved": round(roof["bus_bytes_per_step"] / (ms_step * 1e-3) / 1e9, 1),
+                           "peak": NVLINK_PEER_GBS, "unit": "GB/s",
+                           "frac": roof["step_frac_of_bus_roofline"],
+                           "note": "reduce-scatter + all-gather bus bytes per rank / whole step time"}),
         "e2e": {"value": round(units / (ms_e2e * 1e-3), 1), "unit": "params/s", "ms_per_step": round(ms_e2e, 4),
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "clocks": clk,
