@@ -293,7 +293,7 @@ def run_ours(args):
                 "peak_source": peak_note}
     else:
         bus = (P - 1) / P * (gbytes + 4) * h.padded_numel
-        if fused:  # F1 (reduce+norms) + FX + F2 (update+gather): the transfers ARE these kernels
+        if fused:  # F1 (reduce+norms) + F2 (update+gather): the transfers ARE these kernels
             coll_ms = ph["norms"] + ph["skip_allreduce"] + ph["update"]
             kname = "fused NVLink path: F1 reduce+norms, F2 update+gather"
         else:

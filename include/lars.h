@@ -271,7 +271,9 @@ lars_status_t dp_allreduce_lars_step_host_grad(lars_handle_t h, float* w, const 
  * lars_profile_enable(h, 0) stops. lars_profile_read synchronizes and returns accumulated milliseconds per
  * phase since enable: ms[0] reduce-scatter (C1), ms[1] norms (K1), ms[2] skip/split allreduce (C3 +
  * finisher), ms[3] update (K2), ms[4] all-gather (C2); single-GPU steps fill ms[1] and ms[3]; the fused
- * data-parallel path fills ms[1] (F1: reduce + norms), ms[2] (FX) and ms[3] (F2: update + gather).
+ * data-parallel path fills ms[1] (F1: reduce + norms) and ms[3] (F2: update + gather; the skip/split exchange
+ * lives inside F1's tail and F2's head). Profiling records events between the kernels, which suspends the
+ * programmatic overlap of F1 and F2: the per-phase sum exceeds an unprofiled step.
  * *steps = steps timed. */
 lars_status_t lars_profile_enable(lars_handle_t h, int32_t enable);
 lars_status_t lars_profile_read(lars_handle_t h, double* ms, int64_t* steps);
@@ -279,10 +281,11 @@ lars_status_t lars_profile_read(lars_handle_t h, double* ms, int64_t* steps);
 /* The library-owned weight (fp32) and gradient (grad_dtype) buffers of the FUSED data-parallel path:
  * padded_numel elements each, in NCCL symmetric memory (ncclMemAlloc + window registration) so every rank
  * reaches every other rank's buffers over NVLink. When dp_allreduce_lars_step is given exactly these two
- * pointers it runs three kernels instead of NCCL collectives + two kernels: F1 sums this rank's shard of the
- * gradient over all ranks (fp32, rank order) while computing the layer norms, FX exchanges the skip flag and
- * split-layer sums, F2 updates the shard and stores every new weight into every rank's buffer (the
- * all-gather). Available after lars_comm_init when all ranks share one NVLink domain (NCCL LSA team = world)
+ * pointers it runs two kernels instead of NCCL collectives + three kernels: F1 sums this rank's shard of the
+ * gradient over all ranks (fp32, rank order, peer loads over NVLink) while computing the layer norms, and its
+ * last CTA publishes the skip flag and split-layer sums into every rank's exchange slot; F2 collects them,
+ * updates the shard and stores every new weight into every rank's buffer (the all-gather). One LSA barrier
+ * at F1's entry (every rank's gradient is complete) and one at F2's exit (every rank's weights are). Available after lars_comm_init when all ranks share one NVLink domain (NCCL LSA team = world)
  * and LARS_DP_FUSED is not "0"; otherwise LARS_ERR_NO_COMM. Other pointers keep the NCCL path. */
 lars_status_t lars_dp_buffers(lars_handle_t h, float** w, void** g);
 

@@ -37,18 +37,6 @@ constexpr int kCtasPerSm = LARS_NORM_CTAS_PER_SM;      // K1 resident CTAs per S
 #define LARS_DP_CTAS2 4
 #endif
 constexpr int dp_norm_ctas_per_sm(int nranks) { return nranks <= 2 ? LARS_DP_CTAS2 : 2; }
-#ifndef LARS_DP_TILES_PER_CTA
-#define LARS_DP_TILES_PER_CTA 1
-#endif
-constexpr int kDpTilesPerCta = LARS_DP_TILES_PER_CTA;  // fused F1/F2: tiles per CTA
-#ifndef LARS_NORM_TILES_PER_CTA
-#define LARS_NORM_TILES_PER_CTA 1
-#endif
-#ifndef LARS_NORM_DYNAMIC
-#define LARS_NORM_DYNAMIC 0
-#endif
-constexpr int kTilesPerCta = LARS_NORM_TILES_PER_CTA;  // K1 tiles per persistent CTA
-constexpr bool kNormDynamic = LARS_NORM_DYNAMIC != 0;  // K1 tiles from a ticket counter
 constexpr int32_t kMaxTileChunks = 256; // chunk partials of one tile live in shared memory
 constexpr int32_t kUpdateSplit = 4;     // K2 walks each tile in 4 parts, last part first
 constexpr int kNormUnroll = LARS_NORM_UNROLL;  // K1 vector groups per lane per iteration
@@ -149,10 +137,6 @@ struct DevWork {
 };
 
 struct DevScratch {
-  // Tile tickets of K1 ([0], kNormDynamic only; [1] spare): monotonically increasing, never reset. A
-  // launch performs exactly ntiles + grid fetches (one failing fetch per CTA), so ticket % (ntiles + grid)
-  // is the tile index within the launch — CUDA-graph safe, no per-step memset.
-  unsigned long long* ticket;
   double* cpart_w;       // per chunk: sum w^2 of the chunk
   double* cpart_wnext;   // per chunk: sum w_new^2 written by K2 in carry mode (LARS_FLAG_CARRY_WNORM)
   int32_t* wnext_valid;  // 1 when cpart_wnext describes the current w (set by K2, cleared by the host)
@@ -204,9 +188,8 @@ struct DpFused {
   bool mcast;                     // NVLS multicast all-gather (multimem.st) instead of per-peer stores
   int np_template;                // F1 peer-count template bound (>= nranks; 2, 4 or 8)
 };
-// F1 (reduce + norms, grid_norm CTAs), FX (exchange + finish), F2 (update + gather, grid_update CTAs);
-// both grids identical on every rank (the per-CTA LSA barriers pair CTA b with CTA b of every rank).
-// Events (optional) are recorded after F1 and FX.
+// F1 (reduce + norms + share publication, grid_norm CTAs), then F2 (share collection + update + gather,
+// grid_update CTAs, programmatic dependent launch). Events (optional, profiling) are recorded after F1.
 cudaError_t launch_dp_fused(int32_t grad_dtype, const DevWork& wk, const DevScratch& sc, const Hyper& hy, float* w,
                             float* m, const DpFused& f, int grid_norm, int grid_update, cudaStream_t stream,
                             cudaEvent_t ev1, cudaEvent_t ev2);

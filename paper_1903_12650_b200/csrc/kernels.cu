@@ -483,18 +483,12 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
   }
 }
 
-// Ticket counters are monotonic (never reset): one launch draws exactly nitems + grid tickets (one
-// failing draw per CTA), so ticket % (nitems + grid) is the item index within the launch.
-__device__ __forceinline__ int32_t take_ticket(unsigned long long* t, int32_t nitems, int32_t grid) {
-  return (int32_t)(atomicAdd(t, 1ull) % (unsigned long long)(nitems + grid));
-}
-
 // K1 body, shared by the single-GPU / NCCL kernel and the fused data-parallel kernel (they differ only
-// in where the gradient comes from). Persistent schedule: static (CTA b owns tiles b, b + grid, ...) or
-// dynamic (kNormDynamic).
+// in where the gradient comes from). Static persistent schedule: CTA b owns tiles b, b + grid, ... (one
+// tile per resident CTA by construction of the work list; dynamically scheduled tiles measured slower).
 // Returns true on thread 0 of the CTA that completed the step's layer count (data-parallel mode: the
 // caller then publishes this rank's C3 shares).
-template <bool CARRY, class GL, bool DYN = kNormDynamic>
+template <bool CARRY, class GL>
 __device__ __forceinline__ bool norms_body(const DevWork& wk, const DevScratch& sc, const Hyper& hy,
                                            const float* __restrict__ w, const GL& gl) {
   __shared__ double sm_cw[kMaxTileChunks], sm_cg[kMaxTileChunks];
@@ -507,26 +501,9 @@ __device__ __forceinline__ bool norms_body(const DevWork& wk, const DevScratch& 
   // carry mode: the previous K2 left sum(w_new^2) per chunk; valid until the host invalidates it
   const bool carried = CARRY && *(volatile const int32_t*)sc.wnext_valid != 0;
   const StepLr slr = step_lr(hy);
-  if (DYN) {  // tiles handed out by a ticket counter (faster CTAs take more tiles)
-    __shared__ int32_t s_tile;
-    if (threadIdx.x == 0) s_tile = take_ticket(sc.ticket + 0, wk.ntiles, gridDim.x);
-    __syncthreads();
-    int32_t tile = s_tile;
-    while (tile < wk.ntiles) {
-      __syncthreads();  // s_tile read by all; shared chunk partials of the previous tile consumed
-      int32_t next = 0;
-      if (threadIdx.x == 0) next = take_ticket(sc.ticket + 0, wk.ntiles, gridDim.x);
-      norms_tile(tile, wk, sc, hy, w, gl, sm_cw, sm_cg, &sm_done, &sm_nonfinite, carried, slr);
-      __syncthreads();
-      if (threadIdx.x == 0) s_tile = next;
-      __syncthreads();
-      tile = s_tile;
-    }
-  } else {
-    for (int32_t tile = blockIdx.x; tile < wk.ntiles; tile += gridDim.x) {
-      __syncthreads();  // shared chunk partials of the previous tile fully consumed
-      norms_tile(tile, wk, sc, hy, w, gl, sm_cw, sm_cg, &sm_done, &sm_nonfinite, carried, slr);
-    }
+  for (int32_t tile = blockIdx.x; tile < wk.ntiles; tile += gridDim.x) {
+    __syncthreads();  // shared chunk partials of the previous tile fully consumed
+    norms_tile(tile, wk, sc, hy, w, gl, sm_cw, sm_cg, &sm_done, &sm_nonfinite, carried, slr);
   }
   __syncthreads();
   // Count this CTA's finished layers once; the CTA that completes the count decides the step's skip.
@@ -877,7 +854,7 @@ __global__ void __launch_bounds__(kThreads, dp_norm_ctas_per_sm(NP)) lars_dp_red
   gl.begin = f.begin;
   // static tiles (one per CTA): measured faster than 4x finer dynamically scheduled tiles, whose per-tile
   // overhead outweighs the shorter tail (tools/trace_dp.py)
-  const bool final_cta = norms_body<CARRY, PeerSumGrad<DT, NP>, false>(wk, sc, hy, w, gl);
+  const bool final_cta = norms_body<CARRY, PeerSumGrad<DT, NP>>(wk, sc, hy, w, gl);
   TRACE_MARK(4)
   if (final_cta || (wk.ntensors == 0 && blockIdx.x == 0 && threadIdx.x == 0)) dp_publish_shares(wk, sc, hy, f);
   __syncthreads();

@@ -67,7 +67,6 @@ lars_status_t upload(DevBufs& b, int sms, int32_t nsplit_total, bool dp) {
   add(ns, sizeof(Seg)); add(ntl, 4); add(nt, 4); add(nt, 4); add(nt, 4);                // work list
   add(nc, sizeof(Seg)); add(ntl, 4); add(ns + 1, 4); add(nc, 8); add(nc, 8);            // chunks
   add(nc, 8); add(1, 4);                                                                // carried norms
-  add(2, 8);                                                                            // tickets
   add(nt, 4); add(nt, 4); add(dp ? 1 + 2 * (size_t)nsplit_total : 1, 8);                // split layers, C3
   add(ns, 8); add(ns, 8); add(nt, 4); add(1, 4); add(1, 4); add(1, 4);                  // partials, counters
   add(nt, 8); add(nt, 8); add(nt, 8); add(nt, 4); add(nt, 4);                           // outputs
@@ -83,7 +82,6 @@ lars_status_t upload(DevBufs& b, int sms, int32_t nsplit_total, bool dp) {
   Seg* chunks = carve<Seg>(p, nc);
   int32_t* tile_chunk = carve<int32_t>(p, ntl);
   int32_t* seg_chunk = carve<int32_t>(p, ns + 1);
-  b.sc.ticket = carve<unsigned long long>(p, 2);
   int32_t* tsplit = carve<int32_t>(p, nt);
   int32_t* split_locals = carve<int32_t>(p, nt);
   double* c3 = carve<double>(p, dp ? 1 + 2 * (size_t)nsplit_total : 1);
@@ -377,7 +375,7 @@ lars_status_t lars_init(const lars_tensor_t* tensors, int32_t n, const lars_hpar
     int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0) h->sms = sms;
   }
-  h->full.wl = make_worklist(h->plan, -1, h->sms * kCtasPerSm * kTilesPerCta, min_tile);
+  h->full.wl = make_worklist(h->plan, -1, h->sms * kCtasPerSm, min_tile);
   if (device >= 0) {
     DeviceGuard g(device);
     if (cudaMalloc(&h->lr_d, h->plan.lr.size() * sizeof(double)) != cudaSuccess) { lars_destroy(h); return LARS_ERR_OOM; }
@@ -486,7 +484,7 @@ lars_status_t lars_work_info(lars_handle_t h, int32_t rank, int32_t* ntiles, int
       wl = &h->shard.wl;
     } else {
       const int32_t min_tile = h->hp.tile_elems > 0 ? h->hp.tile_elems : kDefaultMinTile;
-      tmp = make_worklist(h->plan, rank, h->sms * kCtasPerSm * kTilesPerCta, min_tile);
+      tmp = make_worklist(h->plan, rank, h->sms * kCtasPerSm, min_tile);
       wl = &tmp;
     }
   }
@@ -610,7 +608,7 @@ lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, cons
   const int32_t min_tile = h->hp.tile_elems > 0 ? h->hp.tile_elems : kDefaultMinTile;
   const bool fused = fused_eligible(h);
   const int32_t ntiles_target =
-      fused ? h->sms * dp_norm_ctas_per_sm(nranks) * kDpTilesPerCta : h->sms * kCtasPerSm * kTilesPerCta;
+      fused ? h->sms * dp_norm_ctas_per_sm(nranks) : h->sms * kCtasPerSm;
   h->shard.wl = make_worklist(h->plan, rank, ntiles_target, min_tile);
   h->K = std::max(1, h->hp.buckets);
   if (h->K > 1) {
@@ -826,7 +824,7 @@ static lars_status_t dp_impl(lars_handle_t h, float* w, const void* g, float* m,
   lars_status_t cg = carry_guard(h, h->shard, w, s);
   if (cg != LARS_OK) return cg;
   auto* pe = h->prof.begin(2);
-  if (h->fused.ok && (void*)w == h->fused.w && g == h->fused.g) {  // fused NVLink path (F1, FX, F2)
+  if (h->fused.ok && (void*)w == h->fused.w && g == h->fused.g) {  // fused NVLink path (F1, F2)
     DpFused f{h->fused.dc,   h->fused.gwin, h->fused.wwin,  h->fused.xwin,
               h->rank,       h->plan.P,     begin,          h->fused.gred32,
               (unsigned long long*)h->fused.state, (int64_t*)((char*)h->fused.state + 8),
