@@ -250,6 +250,30 @@ def run_ours(args):
         alt["nccl_rs_busbw_GBps"] = round((P - 1) / P * gb / (nph["reduce_scatter"] * 1e-3) / 1e9, 1)
         alt["nccl_ag_busbw_GBps"] = round((P - 1) / P * h.padded_numel * 4 / (nph["all_gather"] * 1e-3) / 1e9, 1)
         alt["nccl_nvls_enable"] = os.environ.get("NCCL_NVLS_ENABLE", "default")
+    if P > 1 and not args.buckets:
+        # LARS_FLAG_HALF_WEIGHTS (NEXT-f3): fp32 masters stay on their shard, the all-gather moves the new
+        # weights in the wire dtype into the compute-weight buffer (half the all-gather bytes)
+        hh = mk((PK.lars.FLAG_CARRY_WNORM if carry else 0) | PK.lars.FLAG_HALF_WEIGHTS)
+        hh.comm_init_torch()
+        wh, gh = w_n.clone(), g_n
+        if fused:
+            wh, gh = hh.dp_buffers()
+            wh.copy_(w_n)
+            gh.copy_(g_n)
+        mh = m.clone()
+        for i in range(args.warmup):
+            hh.dp_allreduce_lars_step(wh, gh, mh, (T0 + i) % T, stream)
+        barrier()
+        torch.cuda.synchronize()
+        e6, e7 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e6.record(stream)
+        for i in range(args.steps):
+            hh.dp_allreduce_lars_step(wh, gh, mh, (T0 + i) % T, stream)
+        e7.record(stream)
+        torch.cuda.synchronize()
+        alt["half_weights_ms_per_step"] = round(max_over_ranks(e6.elapsed_time(e7)) / args.steps, 5)
+        alt["half_weights_path"] = "fused-nvlink" if fused else "nccl"
+        hh.close()
 
     # end to end through the public API with host gradients
     g_pin = torch.from_numpy(G.pack(g_host, h.offsets, h.padded_numel)).pin_memory()  # lands in g's buffer

@@ -139,6 +139,15 @@ typedef enum { LARS_DECAY_POLY = 0, LARS_DECAY_STEP = 1 } lars_decay_t;
  * v <- mu v + lr(t) lambda (s g + beta_l w);  w <- w - v.  Both agree on a step from v = 0. */
 #define LARS_FLAG_LR_AT_APPLY 2u
 
+/* Half-precision compute weights (ZeRO-1 style; "compute and communicate using
+ * half precision ... update own weights using single precision"). P > 1, grad_dtype LARS_F16 or LARS_BF16,
+ * contiguous or LPT shards. Each rank keeps fp32 master weights and momentum for ITS SHARD only; the step's
+ * all-gather moves the new weights rounded to grad_dtype (round to nearest even) into a library-owned
+ * compute-weight buffer (lars_compute_weights), which then holds the full model on every rank, bitwise
+ * identical — half the all-gather bytes of the fp32 default. Elements of w outside this rank's shard are
+ * neither read nor written (they go stale); read the model from the compute-weight buffer instead. */
+#define LARS_FLAG_HALF_WEIGHTS 4u
+
 typedef struct lars_ctx* lars_handle_t;
 
 /* Fills *hp with the defaults listed above (base_lr = 0: the caller must set it). */
@@ -288,6 +297,11 @@ lars_status_t lars_profile_read(lars_handle_t h, double* ms, int64_t* steps);
  * at F1's entry (every rank's gradient is complete) and one at F2's exit (every rank's weights are). Available after lars_comm_init when all ranks share one NVLink domain (NCCL LSA team = world)
  * and LARS_DP_FUSED is not "0"; otherwise LARS_ERR_NO_COMM. Other pointers keep the NCCL path. */
 lars_status_t lars_dp_buffers(lars_handle_t h, float** w, void** g);
+
+/* LARS_FLAG_HALF_WEIGHTS: the library-owned compute-weight buffer (padded_numel elements of grad_dtype, the
+ * lars_layout offsets; valid after the first dp step, rewritten by every step; owned by the library).
+ * LARS_ERR_NO_COMM before lars_comm_init, LARS_ERR_INVALID_ARG without the flag. */
+lars_status_t lars_compute_weights(lars_handle_t h, void** w_half);
 
 /* Device pointer to the reduced gradient shard of the last dp step (S elements of *dtype: the wire dtype on
  * the NCCL path, LARS_F32 on the fused path; first element = global element `begin`). Owned by the library.

@@ -167,6 +167,7 @@ struct Hyper {
   float mu, grad_scale_f;
   bool carry;                // LARS_FLAG_CARRY_WNORM
   bool lr_at_apply;          // LARS_FLAG_LR_AT_APPLY (SPEC.md:186 momentum form)
+  void* w_half = nullptr;    // LARS_FLAG_HALF_WEIGHTS: compute weights (grad dtype) the update also writes
 };
 
 // g_shift: the gradient of flat element e is g[e - g_shift] (the DP step reads its reduced shard).
@@ -187,6 +188,7 @@ struct DpFused {
   unsigned* done;                 // F2 exit: CTAs counted out (the last one syncs with the other ranks)
   bool mcast;                     // NVLS multicast all-gather (multimem.st) instead of per-peer stores
   int np_template;                // F1 peer-count template bound (>= nranks; 2, 4 or 8)
+  ncclWindow_t hwin = nullptr;    // LARS_FLAG_HALF_WEIGHTS: compute-weight window (grad dtype), else null
 };
 // F1 (reduce + norms + share publication, grid_norm CTAs), then F2 (share collection + update + gather,
 // grid_update CTAs, programmatic dependent launch). Events (optional, profiling) are recorded after F1.

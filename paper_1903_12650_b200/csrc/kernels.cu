@@ -591,6 +591,54 @@ struct PeerWeights {
   }
 };
 
+// LARS_FLAG_HALF_WEIGHTS: the new weights rounded to the wire dtype (round to nearest even) go to this
+// rank's compute-weight buffer and (fused path) every other rank's, 16 B per 8 elements.
+template <int HDT>
+__device__ __forceinline__ uint32_t pack2_rn(float a, float b) {
+  if (HDT == LARS_F16) {
+    const __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  }
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+template <int HDT>
+__device__ __forceinline__ uint4 pack8_rn(const F8& x) {
+  return make_uint4(pack2_rn<HDT>(x.v[0], x.v[1]), pack2_rn<HDT>(x.v[2], x.v[3]), pack2_rn<HDT>(x.v[4], x.v[5]),
+                    pack2_rn<HDT>(x.v[6], x.v[7]));
+}
+__device__ __forceinline__ void st16(void* p, uint4 v) {
+  asm volatile("st.global.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+template <int HDT>
+__device__ __forceinline__ uint16_t half_rn(float x) {
+  if (HDT == LARS_F16) {
+    const __half h = __float2half_rn(x);
+    return *reinterpret_cast<const uint16_t*>(&h);
+  }
+  const __nv_bfloat16 h = __float2bfloat16_rn(x);
+  return *reinterpret_cast<const uint16_t*>(&h);
+}
+template <int HDT>
+struct LocalHalf {  // NCCL path: this rank's part of the compute weights (the all-gather follows)
+  uint16_t* wh;
+  __device__ __forceinline__ void store8(int64_t e, const F8& x) const { st16(wh + e, pack8_rn<HDT>(x)); }
+  __device__ __forceinline__ void store1(int64_t e, float x) const { wh[e] = half_rn<HDT>(x); }
+};
+template <int HDT>
+struct PeerHalf {  // fused path: every rank's compute weights, this one's included
+  uint16_t* ph[kMaxRanks];
+  int n;
+  __device__ __forceinline__ void store8(int64_t e, const F8& x) const {
+    const uint4 v = pack8_rn<HDT>(x);
+    for (int p = 0; p < n; ++p) st16(ph[p] + e, v);
+  }
+  __device__ __forceinline__ void store1(int64_t e, float x) const {
+    const uint16_t v = half_rn<HDT>(x);
+    for (int p = 0; p < n; ++p) ph[p][e] = v;
+  }
+};
+
 // NVLS: one multicast store per vector reaches every rank's weight buffer (the NVSwitch replicates it), so
 // the SM issues 1x the bytes instead of (P-1)x. multimem.st is at most 128-bit.
 struct McastWeights {
@@ -688,7 +736,7 @@ __device__ __forceinline__ void update_item(int32_t item, const DevWork& wk, con
 // K2. Same persistent schedule as K1 (CTA b owns tiles b, b + grid, ...; identical grid and resources,
 // so CTA b runs on the same SM in both kernels) and each tile's chunks walked backwards: the gradient
 // bytes K1 streamed last into this SM's L2 slice are re-read first.
-template <int DT, bool CARRY>
+template <int DT, bool CARRY, bool HALF = false>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_update_kernel(DevWork wk, DevScratch sc, Hyper hy,
                                                                            float* __restrict__ w,
                                                                            const void* __restrict__ g,
@@ -700,7 +748,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_update_kernel(DevWo
   if (!skip)
     for (int32_t tile = blockIdx.x; tile < wk.ntiles; tile += gridDim.x)
       for (int32_t q = kUpdateSplit - 1; q >= 0; --q)
-        update_item<DT, CARRY>((kUpdateSplit - 1 - q) * wk.ntiles + tile, wk, sc, hy, w, g, g_shift, m);
+        if constexpr (HALF)
+          update_item<DT, CARRY, LocalHalf<DT>>((kUpdateSplit - 1 - q) * wk.ntiles + tile, wk, sc, hy, w, g,
+                                                g_shift, m, LocalHalf<DT>{(uint16_t*)hy.w_half});
+        else
+          update_item<DT, CARRY>((kUpdateSplit - 1 - q) * wk.ntiles + tile, wk, sc, hy, w, g, g_shift, m);
   // every chunk's sum(w_new^2) is written once this grid completes; the next K1 (stream-ordered after
   // the whole grid) may use them. A skipped step leaves w — and therefore the old sums — valid.
   if (CARRY && !skip && blockIdx.x == 0 && threadIdx.x == 0) *(volatile int32_t*)sc.wnext_valid = 1;
@@ -861,7 +913,7 @@ __global__ void __launch_bounds__(kThreads, dp_norm_ctas_per_sm(NP)) lars_dp_red
   TRACE_END(2)
 }
 
-template <bool CARRY, bool MCAST>
+template <bool CARRY, bool MCAST, int HDT = 0>  // HDT: compute-weight dtype (LARS_FLAG_HALF_WEIGHTS), 0 = fp32 all-gather
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_dp_update_gather_kernel(DevWork wk, DevScratch sc,
                                                                                      Hyper hy, float* w, float* m,
                                                                                      DpFused f) {
@@ -881,7 +933,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_dp_update_gather_ke
   const bool skip = s_status != 0;
   // items ordered last-part-of-every-tile first (see update_item), striped statically over this grid
   if (!skip) {
-    if (MCAST) {
+    if constexpr (HDT != 0) {  // half-precision compute weights to every rank (this one included)
+      PeerHalf<HDT> ws;
+      ws.n = f.nranks;
+      for (int p = 0; p < f.nranks; ++p) ws.ph[p] = (uint16_t*)ncclGetLsaPointer(f.hwin, 0, p);
+      for (int32_t item = blockIdx.x; item < wk.ntiles * kUpdateSplit; item += gridDim.x)
+        update_item<LARS_F32, CARRY, PeerHalf<HDT>>(item, wk, sc, hy, w, f.gred, f.begin, m, ws);
+    } else if (MCAST) {
       const McastWeights ws{(float*)ncclGetLsaMultimemPointer(f.wwin, 0, f.dc)};
       for (int32_t item = blockIdx.x; item < wk.ntiles * kUpdateSplit; item += gridDim.x)
         update_item<LARS_F32, CARRY, McastWeights>(item, wk, sc, hy, w, f.gred, f.begin, m, ws);
@@ -945,7 +1003,15 @@ cudaError_t launch_dp_fused(int32_t dt, const DevWork& wk, const DevScratch& sc,
   launch_reduce_norms(dt, hy.carry, f.np_template, grid_norm, st, wg, sc, hy, w, f);
   if (ev1) cudaEventRecord(ev1, st);
   if (ev2) cudaEventRecord(ev2, st);  // (the exchange now lives inside F1's tail and F2's head)
-  if (hy.carry) {
+  if (f.hwin) {
+    if (dt == LARS_F16) {
+      if (hy.carry) launch_pdl(lars_dp_update_gather_kernel<true, false, LARS_F16>, grid_update, st, wg, sc, hy, w, m, f);
+      else launch_pdl(lars_dp_update_gather_kernel<false, false, LARS_F16>, grid_update, st, wg, sc, hy, w, m, f);
+    } else {
+      if (hy.carry) launch_pdl(lars_dp_update_gather_kernel<true, false, LARS_BF16>, grid_update, st, wg, sc, hy, w, m, f);
+      else launch_pdl(lars_dp_update_gather_kernel<false, false, LARS_BF16>, grid_update, st, wg, sc, hy, w, m, f);
+    }
+  } else if (hy.carry) {
     if (f.mcast) launch_pdl(lars_dp_update_gather_kernel<true, true>, grid_update, st, wg, sc, hy, w, m, f);
     else launch_pdl(lars_dp_update_gather_kernel<true, false>, grid_update, st, wg, sc, hy, w, m, f);
   } else {
@@ -1029,6 +1095,12 @@ static cudaError_t launch_norms_t(const DevWork& wk, const DevScratch& sc, const
 template <int DT>
 static cudaError_t launch_update_t(const DevWork& wk, const DevScratch& sc, const Hyper& hy, float* w,
                                    const void* g, int64_t g_shift, float* m, cudaStream_t st) {
+  if constexpr (DT != LARS_F32) {
+    if (hy.w_half) {
+      if (hy.carry) return launch_pdl(lars_update_kernel<DT, true, true>, wk.grid, st, wk, sc, hy, w, g, g_shift, m);
+      return launch_pdl(lars_update_kernel<DT, false, true>, wk.grid, st, wk, sc, hy, w, g, g_shift, m);
+    }
+  }
   if (hy.carry) return launch_pdl(lars_update_kernel<DT, true>, wk.grid, st, wk, sc, hy, w, g, g_shift, m);
   return launch_pdl(lars_update_kernel<DT, false>, wk.grid, st, wk, sc, hy, w, g, g_shift, m);
 }

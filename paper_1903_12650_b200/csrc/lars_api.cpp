@@ -204,6 +204,10 @@ struct lars_ctx {
   ncclComm_t gcomm = nullptr;    // communicator of the overlapped group reduce-scatters (fewer CTAs)
   std::vector<cudaEvent_t> gev;  // [3*G + 2]: ready[k], rs0[k], rs1[k], then rs_all_done, applied
   bool gtrace = false, gtrace_valid = false;
+  // LARS_FLAG_HALF_WEIGHTS: compute weights (grad dtype, full layout); symmetric when the fused path exists
+  void* whalf = nullptr;
+  bool whalf_nccl_mem = false;
+  ncclWindow_t hwin = nullptr;
 };
 
 // Tile-aligned buckets of ~equal element counts for every rank (the plan is static: every rank derives
@@ -644,6 +648,19 @@ lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, cons
     st = setup_fused(h);
     if (st != LARS_OK) return st;
   }
+  if (h->hp.flags & LARS_FLAG_HALF_WEIGHTS) {
+    const size_t hb = round4k((size_t)h->plan.padded * dtype_size(h->hp.grad_dtype));
+    if (h->fused.ok) {  // peers store into it over NVLink
+      NCCL_OR(ncclMemAlloc(&h->whalf, hb));
+      h->whalf_nccl_mem = true;
+      NCCL_OR(ncclCommWindowRegister(h->comm, h->whalf, hb, &h->hwin, NCCL_WIN_COLL_SYMMETRIC));
+    } else if (cudaMalloc(&h->whalf, hb) != cudaSuccess) {
+      h->whalf = nullptr;
+      return LARS_ERR_OOM;
+    }
+    CUDA_OR(cudaMemset(h->whalf, 0, hb));
+    CUDA_OR(cudaDeviceSynchronize());
+  }
   return LARS_OK;
 }
 
@@ -823,16 +840,19 @@ static lars_status_t dp_impl(lars_handle_t h, float* w, const void* g, float* m,
   const int32_t dt = h->hp.grad_dtype;
   lars_status_t cg = carry_guard(h, h->shard, w, s);
   if (cg != LARS_OK) return cg;
+  Hyper hy_half = hy;
+  hy_half.w_half = h->whalf;  // nullptr unless LARS_FLAG_HALF_WEIGHTS
+  const Hyper& hy2 = hy_half;
   auto* pe = h->prof.begin(2);
   if (h->fused.ok && (void*)w == h->fused.w && g == h->fused.g) {  // fused NVLink path (F1, F2)
     DpFused f{h->fused.dc,   h->fused.gwin, h->fused.wwin,  h->fused.xwin,
               h->rank,       h->plan.P,     begin,          h->fused.gred32,
               (unsigned long long*)h->fused.state, (int64_t*)((char*)h->fused.state + 8),
               (unsigned long long*)((char*)h->fused.state + 16), (unsigned*)((char*)h->fused.state + 24),
-              h->fused.mcast, h->fused.np_template};
+              h->fused.mcast, h->fused.np_template, h->hwin};
     prof_rec(pe, 0, s);
     prof_rec(pe, 1, s);
-    CUDA_OR(launch_dp_fused(dt, h->shard.dw, h->shard.sc, hy, w, m, f, h->fused.grid_norm, h->fused.grid_update, s,
+    CUDA_OR(launch_dp_fused(dt, h->shard.dw, h->shard.sc, hy2, w, m, f, h->fused.grid_norm, h->fused.grid_update, s,
                             pe ? (*pe)[2] : nullptr,
                             pe ? (*pe)[3] : nullptr));
     if (pe) {
@@ -856,9 +876,14 @@ static lars_status_t dp_impl(lars_handle_t h, float* w, const void* g, float* m,
                         h->comm, s));                                                             // C3
   CUDA_OR(launch_split_finish(h->shard.dw, h->shard.sc, hy, s));
   prof_rec(pe, 3, s);
-  CUDA_OR(launch_update(dt, h->shard.dw, h->shard.sc, hy, w, h->gred, begin, m, s));               // K2
+  CUDA_OR(launch_update(dt, h->shard.dw, h->shard.sc, hy2, w, h->gred, begin, m, s));              // K2
   prof_rec(pe, 4, s);
-  NCCL_OR(ncclAllGather(w + begin, w, (size_t)S, ncclFloat32, h->comm, s));                       // C2
+  if (h->whalf) {  // compute weights in the wire dtype: half the all-gather bytes
+    const size_t esz = dtype_size(dt);
+    NCCL_OR(ncclAllGather((const char*)h->whalf + begin * esz, h->whalf, (size_t)S, nccl_type(dt), h->comm, s));
+  } else {
+    NCCL_OR(ncclAllGather(w + begin, w, (size_t)S, ncclFloat32, h->comm, s));                     // C2
+  }
   prof_rec(pe, 5, s);
   h->last_stream = s;
   h->last = &h->shard;
@@ -980,6 +1005,14 @@ lars_status_t lars_dp_buffers(lars_handle_t h, float** w, void** g) {
   return LARS_OK;
 }
 
+lars_status_t lars_compute_weights(lars_handle_t h, void** w_half) {
+  if (!h || !w_half) return LARS_ERR_INVALID_ARG;
+  if (!(h->hp.flags & LARS_FLAG_HALF_WEIGHTS)) return LARS_ERR_INVALID_ARG;
+  if (!h->whalf) return LARS_ERR_NO_COMM;
+  *w_half = h->whalf;
+  return LARS_OK;
+}
+
 lars_status_t lars_reduced_grad(lars_handle_t h, const void** dev_ptr, int32_t* dtype, int64_t* begin, int64_t* end) {
   if (!h || !dev_ptr) return LARS_ERR_INVALID_ARG;
   if (!h->gred) return LARS_ERR_NO_COMM;
@@ -1043,6 +1076,9 @@ lars_status_t lars_destroy(lars_handle_t h) {
       if (f.wwin) ncclCommWindowDeregister(h->comm, f.wwin);
       if (f.gwin) ncclCommWindowDeregister(h->comm, f.gwin);
       if (f.xwin) ncclCommWindowDeregister(h->comm, f.xwin);
+      if (h->hwin) ncclCommWindowDeregister(h->comm, h->hwin);
+      if (h->whalf && h->whalf_nccl_mem) ncclMemFree(h->whalf);
+      if (h->whalf && !h->whalf_nccl_mem) cudaFree(h->whalf);
       if (f.w) ncclMemFree(f.w);
       if (f.g) ncclMemFree(f.g);
       if (f.x) ncclMemFree(f.x);

@@ -32,7 +32,10 @@ lars_status_t validate_hparams(const lars_hparams_t& hp) {
   if (hp.buckets < 0 || hp.buckets > 1024 || hp.reserved != 0) return LARS_ERR_INVALID_ARG;
   if (hp.shard_policy == LARS_SHARD_GROUPS && (hp.group_bytes <= 0 || hp.buckets > 1)) return LARS_ERR_INVALID_ARG;
   if (hp.decay != LARS_DECAY_POLY && hp.decay != LARS_DECAY_STEP) return LARS_ERR_INVALID_ARG;
-  if (hp.flags & ~(LARS_FLAG_CARRY_WNORM | LARS_FLAG_LR_AT_APPLY)) return LARS_ERR_INVALID_ARG;
+  if (hp.flags & ~(LARS_FLAG_CARRY_WNORM | LARS_FLAG_LR_AT_APPLY | LARS_FLAG_HALF_WEIGHTS)) return LARS_ERR_INVALID_ARG;
+  if ((hp.flags & LARS_FLAG_HALF_WEIGHTS) &&
+      (hp.nranks < 2 || hp.grad_dtype == LARS_F32 || hp.shard_policy == LARS_SHARD_GROUPS || hp.buckets > 1))
+    return LARS_ERR_INVALID_ARG;
   if (hp.decay == LARS_DECAY_STEP) {
     if (hp.n_milestones < 0 || hp.n_milestones > 8 || !fin(hp.step_gamma) || hp.step_gamma < 0)
       return LARS_ERR_INVALID_ARG;

@@ -26,6 +26,7 @@ SHARD_POLICY = {"contiguous": 0, "lpt": 1, "groups": 2}
 DECAY = {"poly": 0, "step": 1}
 FLAG_CARRY_WNORM = 1
 FLAG_LR_AT_APPLY = 2
+FLAG_HALF_WEIGHTS = 4  # LARS_FLAG_HALF_WEIGHTS
 
 
 class LarsLibraryMissing(RuntimeError):
@@ -87,6 +88,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "lars_profile_read": (c_int32, [h, POINTER(c_double), POINTER(c_int64)]),
         "lars_reduced_grad": (c_int32, [h, POINTER(c_void_p), POINTER(c_int32), POINTER(c_int64), POINTER(c_int64)]),
         "lars_dp_buffers": (c_int32, [h, POINTER(c_void_p), POINTER(c_void_p)]),
+        "lars_compute_weights": (c_int32, [h, POINTER(c_void_p)]),
         "lars_groups": (c_int32, [h, POINTER(c_int32), POINTER(c_int64), POINTER(c_int64), POINTER(c_int32),
                                   POINTER(c_int32)]),
         "dp_group_ready": (c_int32, [h, c_void_p, c_int32, c_void_p]),
@@ -347,6 +349,16 @@ class Lars:
         g = torch.as_tensor(_DevView(gp.value, self.padded_numel, {"f32": "<f4", "f16": "<f2", "bf16": "<i2"}[
             self.grad_dtype]), device=dev)
         return w, g
+
+    def compute_weights(self):
+        """LARS_FLAG_HALF_WEIGHTS: torch view of the library-owned compute weights (full layout, grad dtype;
+        bf16 viewed as int16 bit patterns)."""
+        import torch
+
+        p = c_void_p()
+        _check(self._lib.lars_compute_weights(self._h, byref(p)), "lars_compute_weights")
+        typestr = {"f16": "<f2", "bf16": "<i2"}[self.grad_dtype]
+        return torch.as_tensor(_DevView(p.value, self.padded_numel, typestr), device=f"cuda:{self.device}")
 
     # ---- readbacks (synchronize) ----
     def last_norms(self):

@@ -116,6 +116,7 @@ def main():
         h.dp_allreduce_lars_step(w, g, m, t)
         torch.cuda.synchronize()
         res = {"name": name, "dtype": dtype, "t": t}
+        half = bool(kw.get("flags", 0) & PK.lars.FLAG_HALF_WEIGHTS)
         if overlap:
             tr = h.group_trace_read()
             ng = len(tr["ready"])
@@ -125,7 +126,10 @@ def main():
             assert tr["applied"] + eps >= max(tr["rs_end"]), tr
             res["groups"] = ng
             res["first_rs_before_backward_end_ms"] = round(tr["ready"][-1] - tr["rs_start"][0], 4)
-        same = all_same(w)  # collectives first: every rank calls them before any rank-local assertion
+        # collectives first: every rank calls them before any rank-local assertion. Half-precision compute
+        # weights: the replicas are the compute-weight buffers (w outside the shard is stale by design).
+        w16 = h.compute_weights() if half else None
+        same = all_same(w16) if half else all_same(w)
         red_t, b, e = h.reduced_grad()
         red_dtype = {torch.float32: "f32", torch.float16: "f16", torch.int16: "bf16"}[red_t.dtype]
         if red_t.dtype == torch.int16:  # bf16 bit patterns travel as fp16 words (bit-preserving)
@@ -162,6 +166,18 @@ def main():
         res["split_layers_here"] = sum(1 for l in mine if pieces[l] != (0, sizes[l]))
         wg = G.unpack(from_dev(w), h.offsets, sizes)
         mg = G.unpack(from_dev(m), h.offsets, sizes)
+        if half:  # this rank's part of the compute weights is its new fp32 master rounded to nearest even
+            w16_h = from_dev(w16)
+            for l, (lo, hi) in pieces.items():
+                mw = wg[l][lo:hi].astype(np.float32)
+                if dtype == "f16":
+                    want16 = mw.astype(np.float16).view(np.uint16)
+                else:
+                    u = mw.view(np.uint32).astype(np.uint64)
+                    want16 = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+                got16 = w16_h[h.offsets[l] + lo: h.offsets[l] + hi].view(np.uint16)
+                assert np.array_equal(got16, want16), f"{name}: compute weights != RNE(master) in tensor {l}"
+            res["half_weights_checked"] = True
         if inject_nan:
             assert status == 1, f"{name}: rank {rank} did not skip although rank 1 had a NaN"
             for l in mine:
@@ -234,6 +250,13 @@ def main():
               dict(inject_nan="split", fused=True)),
              ("nan-in-split-layer", LY.skew1b("zipf", n_tensors=50, total=1_000_000), "f16", 100,
               dict(inject_nan="split")),
+             # half-precision compute weights (NEXT-f3, ZeRO-1 style all-gather in the wire dtype)
+             ("r50-f16-halfw", lay_r50, "f16", 719, dict(flags=4)),
+             ("fused-r50-f16-halfw-carry", lay_r50, "f16", 720, dict(fused=True, flags=5)),
+             ("fused-random-bf16-halfw", LY.random_layout(np.random.default_rng(8), 29), "bf16", 700,
+              dict(fused=True, flags=4)),
+             ("lpt-zipf-bf16-halfw", LY.skew1b("zipf", n_tensors=200, total=4_000_000), "bf16", 500,
+              dict(flags=4, shard_policy="lpt")),
              # static backward-order groups (NEXT-f2)
              ("groups-r50-f16", lay_r50, "f16", 719, dict(shard_policy="groups", group_bytes=4 << 20)),
              ("groups-r50-int-overlap", lay_r50, "f16", 80, dict(kind="integer", shard_policy="groups",
