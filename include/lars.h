@@ -237,7 +237,9 @@ lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, cons
  *   K1 + K2 on the rank's shard only (m is shard-owned: only [begin, end) is read and written)
  *   C2 all-gather:      every rank receives all updated fp32 weights (in place in w)
  * g (the rank's local full gradient) is NOT modified. On completion (stream-ordered) w is bitwise
- * identical on all ranks. Collective: every rank must call it with the same iter. */
+ * identical on all ranks (with LARS_FLAG_HALF_WEIGHTS: the compute-weight buffers are, and w is current on
+ * this rank's shard only). When w and g are the lars_dp_buffers pointers, the fused NVLink kernels replace
+ * C1/K1/K2/C2 (same results, fp32 sums). Collective: every rank must call it with the same iter. */
 lars_status_t dp_allreduce_lars_step(lars_handle_t h, float* w, const void* g, float* m, int64_t iter,
                                      void* stream);
 
