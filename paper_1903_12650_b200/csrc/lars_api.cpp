@@ -832,6 +832,29 @@ lars_status_t lars_group_trace_read(lars_handle_t h, void* ref_event, double* re
   return LARS_OK;
 }
 
+// Device-side view of the fused path's state for one launch. The 64-byte state block holds, in order: the
+// step epoch, the step's iteration, F1's entry "go" flag and F2's exit counter.
+static DpFused fused_view(lars_handle_t h, int64_t begin) {
+  DpFused f{};
+  f.dc = h->fused.dc;
+  f.gwin = h->fused.gwin;
+  f.wwin = h->fused.wwin;
+  f.xwin = h->fused.xwin;
+  f.rank = h->rank;
+  f.nranks = h->plan.P;
+  f.begin = begin;
+  f.gred = h->fused.gred32;
+  char* st = (char*)h->fused.state;
+  f.epoch = (unsigned long long*)st;
+  f.step_iter = (int64_t*)(st + 8);
+  f.go = (unsigned long long*)(st + 16);
+  f.done = (unsigned*)(st + 24);
+  f.mcast = h->fused.mcast;
+  f.np_template = h->fused.np_template;
+  f.hwin = h->hwin;
+  return f;
+}
+
 static lars_status_t dp_impl(lars_handle_t h, float* w, const void* g, float* m, const Hyper& hy, void* stream) {
   if (!h->comm || !h->shard_ready) return LARS_ERR_NO_COMM;
   DeviceGuard dg(h->device);
@@ -845,11 +868,7 @@ static lars_status_t dp_impl(lars_handle_t h, float* w, const void* g, float* m,
   const Hyper& hy2 = hy_half;
   auto* pe = h->prof.begin(2);
   if (h->fused.ok && (void*)w == h->fused.w && g == h->fused.g) {  // fused NVLink path (F1, F2)
-    DpFused f{h->fused.dc,   h->fused.gwin, h->fused.wwin,  h->fused.xwin,
-              h->rank,       h->plan.P,     begin,          h->fused.gred32,
-              (unsigned long long*)h->fused.state, (int64_t*)((char*)h->fused.state + 8),
-              (unsigned long long*)((char*)h->fused.state + 16), (unsigned*)((char*)h->fused.state + 24),
-              h->fused.mcast, h->fused.np_template, h->hwin};
+    const DpFused f = fused_view(h, begin);
     prof_rec(pe, 0, s);
     prof_rec(pe, 1, s);
     CUDA_OR(launch_dp_fused(dt, h->shard.dw, h->shard.sc, hy2, w, m, f, h->fused.grid_norm, h->fused.grid_update, s,
