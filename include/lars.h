@@ -321,6 +321,9 @@ lars_status_t lars_invalidate_carried_norms(lars_handle_t h);
 /* *skipped: 0 = applied, 1 = skipped (non-finite norm), 2 = skipped (device iteration out of range). */
 lars_status_t lars_last_step_skipped(lars_handle_t h, int32_t* skipped);
 
+/* Frees everything the handle owns (device buffers, NCCL communicator, symmetric windows). Destroy (or reset)
+ * any CUDA graph that captured this handle's steps first: an NCCL communicator referenced by a live graph
+ * cannot be torn down. */
 lars_status_t lars_destroy(lars_handle_t h);
 const char* lars_strerror(lars_status_t s);
 const char* lars_version(void);

@@ -72,7 +72,8 @@ def main():
             if k < early:
                 h.dp_group_ready(g, k)
 
-    def run_case(name, lay, dtype, t, kind="random", inject_nan=False, fused=False, overlap=None, **hpkw):
+    def run_case(name, lay, dtype, t, kind="random", inject_nan=False, fused=False, overlap=None, graph=False,
+                 **hpkw):
         kw = hp_kwargs(grad_dtype=dtype, grad_scale=1.0 / (G.GRAD_PRESCALE * P), **hpkw)
         h = PK.Lars([(x.numel, x.kind) for x in lay], device=local, nranks=P, **kw)
         h._policy = kw.get("shard_policy", "contiguous")
@@ -113,7 +114,36 @@ def main():
                 assert e.status == 1, e
             h.group_trace_enable(True)
             backward_then_ready(h, g_before, g, ng if overlap == "all" else ng // 2)
-        h.dp_allreduce_lars_step(w, g, m, t)
+        if graph:  # the step captured once in a CUDA graph with a device-resident iteration, then replayed
+            # one eager step first (NCCL sets up its connections lazily, outside any capture), then the
+            # pre-step state is restored and the carried norms forgotten
+            w_keep, m_keep = w.clone(), m.clone()
+            h.dp_allreduce_lars_step(w, g, m, t)
+            torch.cuda.synchronize()
+            w.copy_(w_keep)
+            m.copy_(m_keep)
+            h.invalidate_carried_norms()
+            torch.cuda.synchronize()
+            it_dev = torch.tensor([t], dtype=torch.int64, device=dev)
+            side = torch.cuda.Stream(device=dev)
+            gr = torch.cuda.CUDAGraph()
+            torch.cuda.synchronize()
+            dbg = os.environ.get("DP_DEBUG")
+            if dbg:
+                print(f"[{rank}] {name}: capture", flush=True)
+            with torch.cuda.graph(gr, stream=side, capture_error_mode="thread_local"):
+                h.dp_allreduce_lars_step_dev_iter(w, g, m, it_dev, stream=side)
+            if dbg:
+                print(f"[{rank}] {name}: replay", flush=True)
+            gr.replay()
+            torch.cuda.synchronize()
+            gr.reset()  # release the graph before the handle (and its NCCL communicator) can be destroyed
+            torch.cuda.synchronize()
+            if dbg:
+                print(f"[{rank}] {name}: replayed it={int(it_dev.item())}", flush=True)
+            assert int(it_dev.item()) == t + 1, "the device iteration did not advance"
+        else:
+            h.dp_allreduce_lars_step(w, g, m, t)
         torch.cuda.synchronize()
         res = {"name": name, "dtype": dtype, "t": t}
         half = bool(kw.get("flags", 0) & PK.lars.FLAG_HALF_WEIGHTS)
@@ -250,6 +280,9 @@ def main():
               dict(inject_nan="split", fused=True)),
              ("nan-in-split-layer", LY.skew1b("zipf", n_tensors=50, total=1_000_000), "f16", 100,
               dict(inject_nan="split")),
+             # one step captured in a CUDA graph (device iteration), NCCL and fused paths
+             ("r50-f16-graph", lay_r50, "f16", 719, dict(graph=True)),
+             ("fused-r50-f16-carry-graph", lay_r50, "f16", 1439, dict(fused=True, flags=1, graph=True)),
              # half-precision compute weights (NEXT-f3, ZeRO-1 style all-gather in the wire dtype)
              ("r50-f16-halfw", lay_r50, "f16", 719, dict(flags=4)),
              ("fused-r50-f16-halfw-carry", lay_r50, "f16", 720, dict(fused=True, flags=5)),
