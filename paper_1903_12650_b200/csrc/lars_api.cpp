@@ -287,7 +287,7 @@ static lars_status_t setup_fused(lars_ctx* h) {
   NCCL_OR(ncclCommWindowRegister(h->comm, f.w, wb, &f.wwin, NCCL_WIN_COLL_SYMMETRIC));
   NCCL_OR(ncclCommWindowRegister(h->comm, f.g, gb, &f.gwin, NCCL_WIN_COLL_SYMMETRIC));
   NCCL_OR(ncclCommWindowRegister(h->comm, f.x, xb, &f.xwin, NCCL_WIN_COLL_SYMMETRIC));
-  // one resident wave each: F1 CTAs spin on CTA 0's go flag, so the whole grid must fit at once
+  // one resident wave each (one tile per CTA); CTA 0 of F1, dispatched first, releases the others
   f.grid_norm = h->sms * dp_norm_ctas_per_sm(h->plan.P);
   f.grid_update = h->sms * kCtasPerSm;
   ncclDevCommRequirements reqs;
