@@ -17,9 +17,12 @@
  *   G      = s * sum_r g_r                                 (s = hp.grad_scale; sum over P ranks)
  *   lr(t)  = base*(t+1)/W  (t < W);  base*((T-t)/(T-W))^p  (W <= t < T)
  *   lambda = eta*||w_l|| / (||G_l|| + beta*||w_l|| + eps)  for weight-kind tensors when ||w_l|| > 0
- *            and the denominator > 0; otherwise 1.  Skip kinds (bias, BN gamma/beta): lambda = 1, beta_l = 0.
+ *            and the denominator exceeds eps; otherwise 1.  Skip kinds (bias, BN gamma/beta):
+ *            lambda = 1, beta_l = 0.
  *   v      <- mu*v + lr(t)*lambda*(G + beta_l*w);   w <- w - v
  *   If any ||w_l|| or ||G_l|| is non-finite the whole step is skipped: w and m are left bitwise unchanged.
+ *   The rank sum is a value in the gradient wire dtype (reading #29): an element whose sum
+ *   overflows grad_dtype (|sum| >= 65520 for fp16) is infinite, so such a step is skipped too.
  *
  * Conventions for every entry point:
  *   * Pointers named w, g, m are CUDA DEVICE pointers on the handle's device unless the name ends in _host.
@@ -53,7 +56,7 @@ typedef enum {
   LARS_ERR_CUDA = 5,        /* a CUDA runtime call failed                                           */
   LARS_ERR_NCCL = 6,        /* an NCCL call failed                                                  */
   LARS_ERR_OOM = 7,         /* device or host allocation failed                                     */
-  LARS_ERR_NO_COMM = 8,     /* dp step before lars_comm_init, or comm init on a P=1 handle          */
+  LARS_ERR_NO_COMM = 8,     /* dp step before lars_comm_init (or no fused/half-weight buffers)      */
   LARS_ERR_NO_DEVICE = 9    /* a device operation on a host-only (device = -1) handle               */
 } lars_status_t;
 
@@ -140,7 +143,7 @@ typedef enum { LARS_DECAY_POLY = 0, LARS_DECAY_STEP = 1 } lars_decay_t;
 #define LARS_FLAG_LR_AT_APPLY 2u
 
 /* Half-precision compute weights (ZeRO-1 style; "compute and communicate using
- * half precision ... update own weights using single precision"). P > 1, grad_dtype LARS_F16 or LARS_BF16,
+ * half precision ... update own weights using single precision"). grad_dtype LARS_F16 or LARS_BF16,
  * contiguous or LPT shards. Each rank keeps fp32 master weights and momentum for ITS SHARD only; the step's
  * all-gather moves the new weights rounded to grad_dtype (round to nearest even) into a library-owned
  * compute-weight buffer (lars_compute_weights), which then holds the full model on every rank, bitwise
@@ -227,9 +230,11 @@ lars_status_t lars_step_host_grad(lars_handle_t h, float* w, const void* g_host,
 /* 128-byte NCCL unique id for lars_comm_init (rank 0 creates it; the caller broadcasts it). */
 lars_status_t lars_get_unique_id(void* id128);
 
-/* Creates the NCCL communicator for this handle (nranks must equal hp.nranks > 1), checks that every
- * rank planned the same layout (hash min == max over ranks, else LARS_ERR_LAYOUT), and allocates the
- * reduced-gradient shard buffer. Collective: every rank must call it. */
+/* Creates the NCCL communicator for this handle (nranks must equal hp.nranks, else LARS_ERR_INVALID_ARG),
+ * checks that every rank planned the same layout (hash min == max over ranks, else LARS_ERR_LAYOUT), and
+ * allocates the reduced-gradient shard buffer (and, when eligible, the fused path's symmetric buffers).
+ * nranks = 1 is valid: a one-rank communicator runs every data-parallel kernel and collective on one GPU.
+ * Collective: every rank must call it. */
 lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, const void* id128);
 
 /* Data-parallel step on rank `rank` (P = hp.nranks):
@@ -296,14 +301,22 @@ lars_status_t lars_profile_read(lars_handle_t h, double* ms, int64_t* steps);
  * gradient over all ranks (fp32, rank order, peer loads over NVLink) while computing the layer norms, and its
  * last CTA publishes the skip flag and split-layer sums into every rank's exchange slot; F2 collects them,
  * updates the shard and stores every new weight into every rank's buffer (the all-gather). One LSA barrier
- * at F1's entry (every rank's gradient is complete) and one at F2's exit (every rank's weights are). Available after lars_comm_init when all ranks share one NVLink domain (NCCL LSA team = world)
+ * at F1's entry (every rank's gradient is complete) and one at F2's exit (every rank's weights are). F1 is a
+ * cooperative launch (its CTAs wait for CTA 0's barrier, so the grid is guaranteed co-resident). Available after lars_comm_init when all ranks share one NVLink domain (NCCL LSA team = world)
  * and LARS_DP_FUSED is not "0"; otherwise LARS_ERR_NO_COMM. Other pointers keep the NCCL path. */
 lars_status_t lars_dp_buffers(lars_handle_t h, float** w, void** g);
 
 /* LARS_FLAG_HALF_WEIGHTS: the library-owned compute-weight buffer (padded_numel elements of grad_dtype, the
- * lars_layout offsets; valid after the first dp step, rewritten by every step; owned by the library).
- * LARS_ERR_NO_COMM before lars_comm_init, LARS_ERR_INVALID_ARG without the flag. */
+ * lars_layout offsets; owned by the library). It holds RNE(w) once seeded by lars_init_weights or
+ * lars_publish_compute_weights (after lars_comm_init), and after every dp step, applied or skipped (a skipped
+ * step publishes the unchanged master weights). LARS_ERR_NO_COMM before lars_comm_init, LARS_ERR_INVALID_ARG
+ * without the flag. */
 lars_status_t lars_compute_weights(lars_handle_t h, void** w_half);
+
+/* LARS_FLAG_HALF_WEIGHTS: writes RNE(w) of the WHOLE layout (w: device fp32, padded_numel elements, a full
+ * replica such as every rank holds after loading a checkpoint) into this rank's compute-weight buffer on
+ * `stream`. LARS_ERR_NO_COMM before lars_comm_init, LARS_ERR_INVALID_ARG without the flag. */
+lars_status_t lars_publish_compute_weights(lars_handle_t h, const float* w, void* stream);
 
 /* Device pointer to the reduced gradient shard of the last dp step (S elements of *dtype: the wire dtype on
  * the NCCL path, LARS_F32 on the fused path; first element = global element `begin`). Owned by the library.

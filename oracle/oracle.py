@@ -107,11 +107,28 @@ def to_double(g) -> np.ndarray:
     return g.astype(np.float64)
 
 
+def wire_overflow_threshold(g) -> float:
+    """Smallest magnitude that rounds (to nearest, ties to even) to infinity in g's wire format: halfway
+    between the largest finite value (2 - 2^-p) 2^emax and 2^(emax+1), i.e. 2^(emax+1) (1 - 2^-(p+2)) for
+    p stored significand bits. fp16 (p = 10, emax = 15): 65520; bf16 (uint16 bit patterns, p = 7,
+    emax = 127): 2^128 (1 - 2^-9); fp32 (p = 23, emax = 127): 2^128 (1 - 2^-25)."""
+    dt = np.asarray(g).dtype
+    p, emax = {np.dtype(np.float16): (10, 15), np.dtype(np.uint16): (7, 127)}.get(dt, (23, 127))
+    return math.ldexp(1.0 - math.ldexp(1.0, -(p + 2)), emax + 1)
+
+
 def combine(g_ranks: list, grad_scale: float) -> np.ndarray:
-    """G = s * sum_r g_r, summed in ascending rank order in float64."""
+    """G = s * sum_r g_r, summed in ascending rank order in float64.
+
+    Reading #29 ("communicate using half precision"): the combined gradient is a value of the
+    wire format, so an element whose exact rank sum rounds to infinity in that format is +-Inf (the step is
+    then skipped, reading #13). A single rank's finite wire values never reach the threshold."""
     total = np.zeros(np.asarray(g_ranks[0]).shape, dtype=np.float64)
     for g in g_ranks:
         total = total + to_double(g)
+    over = np.abs(total) >= wire_overflow_threshold(g_ranks[0])
+    if over.any():
+        total = np.where(over, np.copysign(np.inf, total), total)
     return grad_scale * total
 
 
@@ -137,7 +154,8 @@ def trust_ratio(w_norm: float, g_norm: float, kind: str, eta: float, weight_deca
     if kind != WEIGHT:
         return 1.0, 0.0
     denom = g_norm + weight_decay * w_norm + eps
-    if w_norm > 0.0 and denom > 0.0:
+    # fallback 1 when ||w|| = 0 or the denominator does not exceed the guard (reading #3)
+    if w_norm > 0.0 and denom > eps:
         return eta * w_norm / denom, weight_decay
     return 1.0, weight_decay
 

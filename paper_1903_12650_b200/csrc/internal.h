@@ -192,6 +192,10 @@ struct DpFused {
 };
 // F1 (reduce + norms + share publication, grid_norm CTAs), then F2 (share collection + update + gather,
 // grid_update CTAs, programmatic dependent launch). Events (optional, profiling) are recorded after F1.
+// Resident CTAs per SM of the F1 instance (grad dtype, carry, peer-count template) that will be launched.
+int dp_reduce_norms_blocks_per_sm(int32_t grad_dtype, bool carry, int np_template);
+// Compute weights (grad dtype) of every element of the work list = RNE(w) (LARS_FLAG_HALF_WEIGHTS).
+cudaError_t launch_publish_half(int32_t grad_dtype, const DevWork& wk, const float* w, void* w_half, cudaStream_t stream);
 cudaError_t launch_dp_fused(int32_t grad_dtype, const DevWork& wk, const DevScratch& sc, const Hyper& hy, float* w,
                             float* m, const DpFused& f, int grid_norm, int grid_update, cudaStream_t stream,
                             cudaEvent_t ev1, cudaEvent_t ev2);

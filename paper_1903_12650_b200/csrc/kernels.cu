@@ -187,6 +187,18 @@ struct LocalGrad {
 // Fused data-parallel reduce-scatter (dp fused path): element e of this rank's shard is the sum over the
 // P ranks' gradient buffers (symmetric NCCL window, read over NVLink), accumulated in fp32 in rank order;
 // the sum is also stored once into the local fp32 shard buffer the update kernel reads.
+// Reading #29 (gradients are communicated in half precision): the combined gradient is a
+// wire-format value, so a sum whose magnitude rounds to infinity in the wire dtype IS infinite — the
+// fp32 sum saturates to +-Inf at the wire dtype's round-to-nearest-even overflow threshold, the norm goes
+// non-finite and the whole step is skipped, as on the NCCL path (fp16 sums) and in the oracle.
+template <int DT> struct WireMax { static constexpr float v = 3.4028234663852886e38f; };  // fp32: none
+template <> struct WireMax<LARS_F16> { static constexpr float v = 65520.0f; };  // (65504 + 65536) / 2
+template <> struct WireMax<LARS_BF16> { static constexpr float v = 3.3961775292304958e38f; };  // 0x7F7F8000
+template <int DT>
+__device__ __forceinline__ float wire_saturate(float x) {
+  if constexpr (DT == LARS_F32) return x;
+  return fabsf(x) >= WireMax<DT>::v ? copysignf(__int_as_float(0x7f800000), x) : x;
+}
 constexpr int kMaxRanks = 8;
 template <int DT, int NP>  // NP: compile-time upper bound of the rank count (2, 4 or 8)
 struct PeerSumGrad {
@@ -215,6 +227,8 @@ struct PeerSumGrad {
           for (int i = 0; i < 8; ++i) acc.v[i] += x.v[i];
         }
     }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc.v[i] = wire_saturate<DT>(acc.v[i]);
     st8_noclobber(gred + (e - begin), acc);
     return acc;
   }
@@ -222,6 +236,7 @@ struct PeerSumGrad {
   __device__ __forceinline__ float load1(int64_t e) const {
     float acc = 0.f;
     for (int p = 0; p < nranks; ++p) acc += Grad<DT>::load1(gp[p], e);
+    acc = wire_saturate<DT>(acc);
     gred[e - begin] = acc;
     return acc;
   }
@@ -242,20 +257,27 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // Launch with programmatic dependent launch: the kernel may become resident while its predecessor
-// drains and must call pdl_wait() before touching anything the predecessor writes.
+// drains and must call pdl_wait() before touching anything the predecessor writes. coop: cooperative
+// launch — the driver guarantees every CTA of the grid is co-resident (F1's CTAs wait on CTA 0's flag).
 template <typename K, typename... Args>
-static cudaError_t launch_pdl(K kernel, int grid, cudaStream_t stream, Args... args) {
+static cudaError_t launch_pdl_ex(K kernel, int grid, cudaStream_t stream, bool coop, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = coop ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+template <typename K, typename... Args>
+static cudaError_t launch_pdl(K kernel, int grid, cudaStream_t stream, Args... args) {
+  return launch_pdl_ex(kernel, grid, stream, false, args...);
 }
 
 __device__ __forceinline__ void acc8(double& a, const F8& x) {
@@ -303,7 +325,8 @@ __device__ __forceinline__ bool finish_core(int32_t l, int32_t lars, double sw, 
   if (lars) {  // weight kind: trust ratio + decay (reading #1, #3); skip kinds keep 1, 0 (#4)
     beta = hy.weight_decay;
     const double den = gn + hy.weight_decay * wn + hy.eps;
-    if (wn > 0.0 && den > 0.0) lam = hy.eta * wn / den;
+    // lambda = 1 when ||w|| = 0 or the denominator does not exceed the guard (reading #3)
+    if (wn > 0.0 && den > hy.eps) lam = hy.eta * wn / den;
   }
   sc.w_norm[l] = wn;
   sc.g_norm[l] = gn;
@@ -639,6 +662,22 @@ struct PeerHalf {  // fused path: every rank's compute weights, this one's inclu
   }
 };
 
+// LARS_FLAG_HALF_WEIGHTS on a step that is NOT applied (skipped, or before any applied step): the compute
+// weights must still be RNE(master) — a skipped step publishes the unchanged master weights of the work
+// list, so the all-gather that follows never spreads stale (or initial zero) compute weights.
+template <typename WS>
+__device__ __forceinline__ void publish_half_tiles(const DevWork& wk, const float* __restrict__ w, const WS& ws) {
+  constexpr int kWarps = kThreads / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int32_t tile = blockIdx.x; tile < wk.ntiles; tile += gridDim.x)
+    for (int32_t c = wk.tile_chunk[tile] + warp; c < wk.tile_chunk[tile + 1]; c += kWarps) {
+      const Seg ck = wk.chunks[c];
+      const int32_t ng = ck.len >> 3;
+      for (int32_t j = lane; j < ng; j += 32) ws.store8(ck.begin + 8 * j, ld8_nc(w + ck.begin + 8 * j));
+      for (int32_t i = (ng << 3) + lane; i < ck.len; i += 32) ws.store1(ck.begin + i, w[ck.begin + i]);
+    }
+}
+
 // NVLS: one multicast store per vector reaches every rank's weight buffer (the NVSwitch replicates it), so
 // the SM issues 1x the bytes instead of (P-1)x. multimem.st is at most 128-bit.
 struct McastWeights {
@@ -753,6 +792,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_update_kernel(DevWo
                                                 g_shift, m, LocalHalf<DT>{(uint16_t*)hy.w_half});
         else
           update_item<DT, CARRY>((kUpdateSplit - 1 - q) * wk.ntiles + tile, wk, sc, hy, w, g, g_shift, m);
+  if constexpr (HALF)
+    if (skip) publish_half_tiles(wk, w, LocalHalf<DT>{(uint16_t*)hy.w_half});
   // every chunk's sum(w_new^2) is written once this grid completes; the next K1 (stream-ordered after
   // the whole grid) may use them. A skipped step leaves w — and therefore the old sums — valid.
   if (CARRY && !skip && blockIdx.x == 0 && threadIdx.x == 0) *(volatile int32_t*)sc.wnext_valid = 1;
@@ -931,6 +972,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_dp_update_gather_ke
   __syncthreads();
   TRACE_MARK_AT(4, 0)
   const bool skip = s_status != 0;
+  if constexpr (HDT != 0) {
+    if (skip) {  // the compute weights stay RNE(master) on every rank
+      PeerHalf<HDT> ws;
+      ws.n = f.nranks;
+      for (int p = 0; p < f.nranks; ++p) ws.ph[p] = (uint16_t*)ncclGetLsaPointer(f.hwin, 0, p);
+      publish_half_tiles(wk, w, ws);
+    }
+  }
   // items ordered last-part-of-every-tile first (see update_item), striped statically over this grid
   if (!skip) {
     if constexpr (HDT != 0) {  // half-precision compute weights to every rank (this one included)
@@ -974,12 +1023,37 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_dp_update_gather_ke
 template <int DT, bool CARRY>
 static void launch_reduce_norms_np(int np, int grid, cudaStream_t st, const DevWork& wk, const DevScratch& sc,
                                    const Hyper& hy, const float* w, const DpFused& f) {
+  // cooperative: every CTA waits for CTA 0's entry flag, so the whole grid must be co-resident
   if (np <= 2)
-    launch_pdl(lars_dp_reduce_norms_kernel<DT, CARRY, 2>, grid, st, wk, sc, hy, w, f);
+    launch_pdl_ex(lars_dp_reduce_norms_kernel<DT, CARRY, 2>, grid, st, true, wk, sc, hy, w, f);
   else if (np <= 4)
-    launch_pdl(lars_dp_reduce_norms_kernel<DT, CARRY, 4>, grid, st, wk, sc, hy, w, f);
+    launch_pdl_ex(lars_dp_reduce_norms_kernel<DT, CARRY, 4>, grid, st, true, wk, sc, hy, w, f);
   else
-    launch_pdl(lars_dp_reduce_norms_kernel<DT, CARRY, 8>, grid, st, wk, sc, hy, w, f);
+    launch_pdl_ex(lars_dp_reduce_norms_kernel<DT, CARRY, 8>, grid, st, true, wk, sc, hy, w, f);
+}
+
+template <int DT, bool CARRY>
+static int reduce_norms_occupancy_np(int np) {
+  int n = 0;
+  cudaError_t e;
+  if (np <= 2)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lars_dp_reduce_norms_kernel<DT, CARRY, 2>, kThreads, 0);
+  else if (np <= 4)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lars_dp_reduce_norms_kernel<DT, CARRY, 4>, kThreads, 0);
+  else
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lars_dp_reduce_norms_kernel<DT, CARRY, 8>, kThreads, 0);
+  return e == cudaSuccess ? n : 0;
+}
+
+int dp_reduce_norms_blocks_per_sm(int32_t dt, bool carry, int np) {
+  if (carry) {
+    if (dt == LARS_F32) return reduce_norms_occupancy_np<LARS_F32, true>(np);
+    if (dt == LARS_F16) return reduce_norms_occupancy_np<LARS_F16, true>(np);
+    return reduce_norms_occupancy_np<LARS_BF16, true>(np);
+  }
+  if (dt == LARS_F32) return reduce_norms_occupancy_np<LARS_F32, false>(np);
+  if (dt == LARS_F16) return reduce_norms_occupancy_np<LARS_F16, false>(np);
+  return reduce_norms_occupancy_np<LARS_BF16, false>(np);
 }
 
 static void launch_reduce_norms(int32_t dt, bool carry, int np, int grid, cudaStream_t st, const DevWork& wk,
@@ -1023,6 +1097,20 @@ cudaError_t launch_dp_fused(int32_t dt, const DevWork& wk, const DevScratch& sc,
 
 cudaError_t launch_split_finish(const DevWork& wk, const DevScratch& sc, const Hyper& hy, cudaStream_t st) {
   lars_split_finish_kernel<<<1, 32, 0, st>>>(wk, sc, hy);
+  return cudaGetLastError();
+}
+
+template <int HDT>
+__global__ void __launch_bounds__(kThreads) lars_publish_half_kernel(DevWork wk, const float* __restrict__ w,
+                                                                    uint16_t* __restrict__ wh) {
+  publish_half_tiles(wk, w, LocalHalf<HDT>{wh});
+}
+
+cudaError_t launch_publish_half(int32_t dt, const DevWork& wk, const float* w, void* w_half, cudaStream_t st) {
+  if (wk.ntiles == 0) return cudaSuccess;
+  if (dt == LARS_F16) lars_publish_half_kernel<LARS_F16><<<wk.grid, kThreads, 0, st>>>(wk, w, (uint16_t*)w_half);
+  else if (dt == LARS_BF16) lars_publish_half_kernel<LARS_BF16><<<wk.grid, kThreads, 0, st>>>(wk, w, (uint16_t*)w_half);
+  else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 

@@ -287,8 +287,8 @@ static lars_status_t setup_fused(lars_ctx* h) {
   NCCL_OR(ncclCommWindowRegister(h->comm, f.w, wb, &f.wwin, NCCL_WIN_COLL_SYMMETRIC));
   NCCL_OR(ncclCommWindowRegister(h->comm, f.g, gb, &f.gwin, NCCL_WIN_COLL_SYMMETRIC));
   NCCL_OR(ncclCommWindowRegister(h->comm, f.x, xb, &f.xwin, NCCL_WIN_COLL_SYMMETRIC));
-  // one resident wave each (one tile per CTA); CTA 0 of F1, dispatched first, releases the others
-  f.grid_norm = h->sms * dp_norm_ctas_per_sm(h->plan.P);
+  // one resident wave each (one tile per CTA). F1 is a cooperative launch sized by the occupancy of the
+  // exact instance launched (lars_comm_init computed it); launch_dp_fused caps it at one CTA per tile.
   f.grid_update = h->sms * kCtasPerSm;
   ncclDevCommRequirements reqs;
   std::memset(&reqs, 0, sizeof reqs);
@@ -302,10 +302,6 @@ static lars_status_t setup_fused(lars_ctx* h) {
     NCCL_OR(ncclDevCommCreate(h->comm, &reqs, &f.dc));
   }
   f.mcast = reqs.lsaMultimem;
-  // F1 is instantiated for up to 2, 4 or 8 peers; LARS_DP_NP (test knob) forces a wider instance so the
-  // P = 8 kernel can be exercised on a box with fewer GPUs (absent peers are predicated off)
-  const char* np_env = getenv("LARS_DP_NP");
-  f.np_template = std::min(8, std::max(h->plan.P, np_env ? atoi(np_env) : 0));
   f.dc_ok = true;
   if (cudaMalloc(&f.gred32, (size_t)h->plan.S * sizeof(float)) != cudaSuccess) return LARS_ERR_OOM;
   if (cudaMalloc(&f.state, 64) != cudaSuccess) return LARS_ERR_OOM;
@@ -476,6 +472,19 @@ lars_status_t lars_init_weights(lars_handle_t h, float* w, uint64_t seed, void* 
   CUDA_OR(launch_init_weights(h->full.dw, h->init, w, seed, (cudaStream_t)stream));
   h->full.carry_w = nullptr;  // new weights: any carried norms are stale
   h->shard.carry_w = nullptr;
+  // every rank initializes the whole replica, so it can also write its whole compute-weight copy
+  if (h->whalf) CUDA_OR(launch_publish_half(h->hp.grad_dtype, h->full.dw, w, h->whalf, (cudaStream_t)stream));
+  return LARS_OK;
+}
+
+lars_status_t lars_publish_compute_weights(lars_handle_t h, const float* w, void* stream) {
+  if (!h || !w) return LARS_ERR_INVALID_ARG;
+  if (h->device < 0) return LARS_ERR_NO_DEVICE;
+  if (!(h->hp.flags & LARS_FLAG_HALF_WEIGHTS)) return LARS_ERR_INVALID_ARG;
+  if (!h->whalf) return LARS_ERR_NO_COMM;
+  if (!aligned256(w)) return LARS_ERR_ALIGNMENT;
+  DeviceGuard dg(h->device);
+  CUDA_OR(launch_publish_half(h->hp.grad_dtype, h->full.dw, w, h->whalf, (cudaStream_t)stream));
   return LARS_OK;
 }
 
@@ -584,7 +593,8 @@ lars_status_t lars_get_unique_id(void* id128) {
 lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, const void* id128) {
   if (!h || !id128) return LARS_ERR_INVALID_ARG;
   if (h->device < 0) return LARS_ERR_NO_DEVICE;
-  if (h->plan.P <= 1) return LARS_ERR_NO_COMM;
+  // P = 1 is allowed: a one-rank communicator runs every data-parallel kernel (fused F1/F2, the NCCL
+  // path, groups, buckets, half-precision compute weights) on a single GPU.
   if (nranks != h->plan.P || rank < 0 || rank >= nranks) return LARS_ERR_INVALID_ARG;
   if (h->comm) return LARS_ERR_INVALID_ARG;
   DeviceGuard dg(h->device);
@@ -611,8 +621,19 @@ lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, cons
   if (r[0] != h->plan.hash || r[1] != h->plan.hash) return LARS_ERR_LAYOUT;
   const int32_t min_tile = h->hp.tile_elems > 0 ? h->hp.tile_elems : kDefaultMinTile;
   const bool fused = fused_eligible(h);
-  const int32_t ntiles_target =
-      fused ? h->sms * dp_norm_ctas_per_sm(nranks) : h->sms * kCtasPerSm;
+  int32_t ntiles_target = h->sms * kCtasPerSm;
+  if (fused) {
+    // F1 is instantiated for up to 2, 4 or 8 peers; LARS_DP_NP (test knob) forces a wider instance so the
+    // P = 8 kernel can be exercised on a box with fewer GPUs (absent peers are predicated off). One tile
+    // per resident CTA of the instance that will run.
+    const char* np_env = getenv("LARS_DP_NP");
+    h->fused.np_template = std::min(8, std::max(h->plan.P, np_env ? atoi(np_env) : 0));
+    const int bpsm = dp_reduce_norms_blocks_per_sm(h->hp.grad_dtype, (h->hp.flags & LARS_FLAG_CARRY_WNORM) != 0,
+                                                   h->fused.np_template);
+    if (bpsm <= 0) return LARS_ERR_CUDA;
+    h->fused.grid_norm = h->sms * bpsm;
+    ntiles_target = h->fused.grid_norm;
+  }
   h->shard.wl = make_worklist(h->plan, rank, ntiles_target, min_tile);
   h->K = std::max(1, h->hp.buckets);
   if (h->K > 1) {

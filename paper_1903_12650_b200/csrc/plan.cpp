@@ -34,7 +34,7 @@ lars_status_t validate_hparams(const lars_hparams_t& hp) {
   if (hp.decay != LARS_DECAY_POLY && hp.decay != LARS_DECAY_STEP) return LARS_ERR_INVALID_ARG;
   if (hp.flags & ~(LARS_FLAG_CARRY_WNORM | LARS_FLAG_LR_AT_APPLY | LARS_FLAG_HALF_WEIGHTS)) return LARS_ERR_INVALID_ARG;
   if ((hp.flags & LARS_FLAG_HALF_WEIGHTS) &&
-      (hp.nranks < 2 || hp.grad_dtype == LARS_F32 || hp.shard_policy == LARS_SHARD_GROUPS || hp.buckets > 1))
+      (hp.grad_dtype == LARS_F32 || hp.shard_policy == LARS_SHARD_GROUPS || hp.buckets > 1))
     return LARS_ERR_INVALID_ARG;
   if (hp.decay == LARS_DECAY_STEP) {
     if (hp.n_milestones < 0 || hp.n_milestones > 8 || !fin(hp.step_gamma) || hp.step_gamma < 0)

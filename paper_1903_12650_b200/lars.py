@@ -89,6 +89,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "lars_reduced_grad": (c_int32, [h, POINTER(c_void_p), POINTER(c_int32), POINTER(c_int64), POINTER(c_int64)]),
         "lars_dp_buffers": (c_int32, [h, POINTER(c_void_p), POINTER(c_void_p)]),
         "lars_compute_weights": (c_int32, [h, POINTER(c_void_p)]),
+        "lars_publish_compute_weights": (c_int32, [h, c_void_p, c_void_p]),
         "lars_groups": (c_int32, [h, POINTER(c_int32), POINTER(c_int64), POINTER(c_int64), POINTER(c_int32),
                                   POINTER(c_int32)]),
         "dp_group_ready": (c_int32, [h, c_void_p, c_int32, c_void_p]),
@@ -359,6 +360,11 @@ class Lars:
         _check(self._lib.lars_compute_weights(self._h, byref(p)), "lars_compute_weights")
         typestr = {"f16": "<f2", "bf16": "<i2"}[self.grad_dtype]
         return torch.as_tensor(_DevView(p.value, self.padded_numel, typestr), device=f"cuda:{self.device}")
+
+    def publish_compute_weights(self, w, stream=None) -> None:
+        """LARS_FLAG_HALF_WEIGHTS: compute weights = RNE(w) for the whole layout (w: a full fp32 replica)."""
+        _check(self._lib.lars_publish_compute_weights(self._h, _ptr(w), _stream(stream)),
+               "lars_publish_compute_weights")
 
     # ---- readbacks (synchronize) ----
     def last_norms(self):

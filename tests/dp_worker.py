@@ -84,13 +84,22 @@ def main():
             g_all = [G.integer_grads(lay, r, t, dtype) for r in range(P)]
         else:
             g_all = [G.grads(lay, r, t, dtype) for r in range(P)]
+        expect_skip = bool(inject_nan)
+        if kind in ("overflow", "near-overflow"):  # reading #29: every rank's element is finite in fp16
+            v = 40000.0 if kind == "overflow" else 65504.0 / (2 * P)
+            for r in range(P):
+                g_all[r][0] = g_all[r][0].copy()
+                g_all[r][0][5] = np.float16(v)
+            expect_skip = bool(np.isinf(O.combine([g_all[r][0][5:6] for r in range(P)], 1.0)).any())
+            assert expect_skip == (kind == "overflow" and P > 1)
         if inject_nan:  # rank 1 poisons one element of ITS local gradient
             q, l0, i0 = 1 % P, 0, 3
             if inject_nan == "split":  # ... the last element of a layer that straddles a shard boundary
                 rng0 = owned_ranges(h, 0) + owned_ranges(h, 1 % P)
                 cuts = sorted({e for _, e in rng0} | {b for b, _ in rng0})
-                l0 = next(l for l, x in enumerate(lay)
-                          if any(h.offsets[l] < c < h.offsets[l] + x.numel for c in cuts))
+                # (P = 1: no layer straddles ranks; the last element of layer 0)
+                l0 = next((l for l, x in enumerate(lay)
+                           if any(h.offsets[l] < c < h.offsets[l] + x.numel for c in cuts)), 0)
                 i0 = lay[l0].numel - 1
             g_all[q][l0] = g_all[q][l0].copy()
             g_all[q][l0][i0] = np.nan
@@ -208,8 +217,8 @@ def main():
                 got16 = w16_h[h.offsets[l] + lo: h.offsets[l] + hi].view(np.uint16)
                 assert np.array_equal(got16, want16), f"{name}: compute weights != RNE(master) in tensor {l}"
             res["half_weights_checked"] = True
-        if inject_nan:
-            assert status == 1, f"{name}: rank {rank} did not skip although rank 1 had a NaN"
+        if expect_skip:
+            assert status == 1, f"{name}: rank {rank} did not skip (non-finite / overflowing gradient sum)"
             for l in mine:
                 assert np.array_equal(wg[l], w_l[l]) and np.array_equal(mg[l], m_l[l])
             res["skipped_everywhere"] = True
@@ -244,7 +253,13 @@ def main():
         # this rank's pieces of w and m vs the oracle DP step (exact sum) of the layers it touches
         r_or = O.dp_step([kinds[l] for l in mine], hp, t, [w_l[l] for l in mine],
                          [[g_all[r][l] for l in mine] for r in range(P)], [m_l[l] for l in mine])
-        tol = TOL_F32 if dtype == "f32" else TOL_F16_DP if dtype == "f16" else TOL_BF16_DP
+        # fp32 sums (the fused path, fp32 wire) or P = 1 (nothing summed): the fp32 gate; fp16 / bf16 sums on
+        # the NCCL wire at P > 1: readings #17 / #18
+        if red_dtype == "f32" or P == 1:
+            tol = TOL_F32
+        else:
+            tol = TOL_F16_DP if red_dtype == "f16" else TOL_BF16_DP
+        res["tol"] = tol
         if mine:
             sl = lambda arrs: np.concatenate([a[pieces[l][0]:pieces[l][1]] for a, l in zip(arrs, mine)])
             res["m_err"] = gate(f"{name} m", sl([mg[l] for l in mine]), sl(r_or.m), sl(r_or.m_env), tol)
@@ -269,6 +284,14 @@ def main():
              ("r50-int-buckets8-carry", lay_r50, "f16", 83, dict(kind="integer", buckets=8, flags=1)),
              ("zipf-f16", LY.skew1b("zipf", n_tensors=200, total=4_000_000), "f16", 500, {}),
              ("nan-on-rank1", LY.tiny(), "f16", 100, dict(inject_nan=True)),
+             # reading #29: per-rank finite fp16 gradients whose sum overflows fp16 -> skipped on every path
+             ("overflow-sum-f16", LY.tiny(), "f16", 100, dict(kind="overflow")),
+             ("fused-overflow-sum-f16", LY.tiny(), "f16", 100, dict(kind="overflow", fused=True)),
+             ("near-overflow-sum-f16", LY.tiny(), "f16", 100, dict(kind="near-overflow")),
+             ("fused-near-overflow-sum-f16", LY.tiny(), "f16", 100, dict(kind="near-overflow", fused=True)),
+             # a skipped FIRST step still leaves the compute weights = RNE(master) on every rank
+             ("halfw-nan-first-step", LY.tiny(), "f16", 100, dict(inject_nan=True, flags=4)),
+             ("fused-halfw-nan-first-step", LY.tiny(), "f16", 100, dict(inject_nan=True, flags=4, fused=True)),
              ("fused-tiny-int", LY.tiny(), "f16", 80, dict(kind="integer", fused=True)),
              ("fused-r50-f16", lay_r50, "f16", 719, dict(fused=True)),
              ("fused-r50-f16-carry", lay_r50, "f16", 720, dict(fused=True, flags=1)),
@@ -326,15 +349,17 @@ def main():
     report["parallel_init_identical"] = all_same(w_i)
     assert report["parallel_init_identical"]
     hi.close()
-    # layout disagreement across ranks -> LARS_ERR_LAYOUT on every rank
+    # layout disagreement across ranks -> LARS_ERR_LAYOUT on every rank (needs two ranks)
+    report["layout_mismatch_rejected"] = None if P == 1 else False
     bad = LY.tiny() if rank == 0 else LY.tiny()[:2]
-    h = PK.Lars([(x.numel, x.kind) for x in bad], device=local, nranks=P, **hp_kwargs())
-    try:
-        h.comm_init_torch()
-        raise AssertionError("layout mismatch accepted")
-    except PK.LarsError as e:
-        assert e.status == 2, e
-    report["layout_mismatch_rejected"] = True
+    if P > 1:
+        h = PK.Lars([(x.numel, x.kind) for x in bad], device=local, nranks=P, **hp_kwargs())
+        try:
+            h.comm_init_torch()
+            raise AssertionError("layout mismatch accepted")
+        except PK.LarsError as e:
+            assert e.status == 2, e
+        report["layout_mismatch_rejected"] = True
     dist.barrier()
     out = os.environ.get("DP_REPORT_DIR")
     if out:

@@ -215,7 +215,7 @@ def test_device_argument_errors():
     assert e.value.status == 8
     with pytest.raises(P.LarsError) as e:
         s.h.comm_init(0, 2, bytes(128))
-    assert e.value.status == 8  # planned for nranks = 1
+    assert e.value.status == 1  # planned for nranks = 1: nranks must match the plan
     torch.cuda.synchronize()
 
 

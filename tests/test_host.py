@@ -127,14 +127,16 @@ def test_product_path_does_not_import_oracle():
 
 
 def test_half_weights_flag_validation():
-    """LARS_FLAG_HALF_WEIGHTS needs P > 1 and a 16-bit wire dtype, and excludes the group and bucket schedules."""
+    """LARS_FLAG_HALF_WEIGHTS needs a 16-bit wire dtype and excludes the group and bucket schedules (P = 1 is
+    allowed: a one-rank communicator runs the data-parallel step)."""
     import paper_1903_12650_b200 as PK
     from synth import layouts as LY
 
     lay = [(t.numel, t.kind) for t in LY.tiny()]
     ok = PK.Lars(lay, device=-1, base_lr=1.0, nranks=2, grad_dtype="f16", flags=PK.lars.FLAG_HALF_WEIGHTS)
     assert ok.padded_numel > 0
-    for kw in (dict(nranks=1, grad_dtype="f16"), dict(nranks=2, grad_dtype="f32"),
+    assert PK.Lars(lay, device=-1, base_lr=1.0, nranks=1, grad_dtype="f16", flags=PK.lars.FLAG_HALF_WEIGHTS).n == 3
+    for kw in (dict(nranks=1, grad_dtype="f32"), dict(nranks=2, grad_dtype="f32"),
                dict(nranks=2, grad_dtype="bf16", shard_policy="groups"), dict(nranks=2, grad_dtype="f16", buckets=4)):
         with pytest.raises(PK.LarsError):
             PK.Lars(lay, device=-1, base_lr=1.0, flags=PK.lars.FLAG_HALF_WEIGHTS, **kw)

@@ -96,6 +96,20 @@ def test_p4_trust_ratio_closed_forms():
     assert abs(a - b) <= 1e-12 * a
     # eps enters the denominator
     assert O.trust_ratio(1.0, 1.0, "weight", 1e-3, 0.0, 1.0)[0] == pytest.approx(5e-4, rel=1e-15)
+    # "if w_norm = 0 or denominator <= epsilon_guard, returns 1" — with eps > 0 a zero
+    # gradient of a layer without decay would otherwise get eta*||w||/eps (1e5 for eta = 1e-3, eps = 1e-8)
+    assert O.trust_ratio(1.0, 0.0, "weight", 1e-3, 0.0, 1e-8)[0] == 1.0
+    assert O.trust_ratio(1.0, 0.0, "weight", 1e-3, 5e-5, 1e-8)[0] == pytest.approx(1e-3 / (5e-5 + 1e-8), rel=1e-15)
+
+
+def test_p4_eps_guard_zero_gradient_through_step():
+    """eps > 0, g = 0, beta = 0 on a weight-kind layer: lambda = 1, so the update is exactly
+    v = mu*m (no gradient, no decay) — not a 1e5-fold step."""
+    w = [np.full(16, 0.25, np.float32)]
+    m = [np.full(16, 2.0 ** -10, np.float32)]
+    r = O.step(["weight"], hp(eps=1e-8, weight_decay=0.0), 100, w, [[np.zeros(16, np.float32)]], m)
+    assert r.lam == [1.0] and not r.skipped
+    assert np.array_equal(r.m[0], np.full(16, 0.9 * 2.0 ** -10)) and np.array_equal(r.w[0], 0.25 - r.m[0])
 
 
 def test_p4d_constant_tensors_through_step():
@@ -233,6 +247,42 @@ def test_p10_rank_sum_brute_force():
         gr = [(rng.standard_normal(37)).astype(np.float16) for _ in range(P)]
         exact = [sum(Fraction(float(g[i])) for g in gr) for i in range(37)]
         assert O.combine(gr, 1.0).tolist() == [float(e) for e in exact]  # exact in double (O2)
+
+
+def test_wire_overflow_thresholds_match_format_rounding():
+    """Reading #29: the threshold is the smallest magnitude the format's round-to-nearest-even sends to
+    infinity. Checked against numpy's own double -> fp16 / fp32 conversions and a bit-level fp32 -> bf16 RNE."""
+    t16 = O.wire_overflow_threshold(np.zeros(1, np.float16))
+    assert t16 == 65520.0
+    assert np.isinf(np.float16(t16)) and np.float16(np.nextafter(t16, 0.0)) == 65504.0
+    t32 = O.wire_overflow_threshold(np.zeros(1, np.float32))
+    assert np.isinf(np.float32(t32)) and np.isfinite(np.float32(np.nextafter(t32, 0.0)))
+    tb = O.wire_overflow_threshold(np.zeros(1, np.uint16))
+    u = int(np.float32(tb).view(np.uint32))
+    assert float(np.float32(tb)) == tb and u == 0x7F7F8000
+    rne = lambda x: (x + 0x7FFF + ((x >> 16) & 1)) >> 16
+    assert rne(u) == 0x7F80 and rne(u - 1) == 0x7F7F  # inf at the threshold, max finite just below
+
+
+def test_wire_overflow_of_rank_sum_skips_step():
+    """Reading #29: per-rank finite fp16 gradients whose exact sum overflows fp16 are an infinite combined
+    gradient -> the whole step is skipped; a sum that stays below the threshold is applied."""
+    kinds = ["weight", "bn_gamma"]
+    w = [np.full(8, 0.5, np.float32), np.ones(3, np.float32)]
+    m = [np.zeros(8, np.float32), np.zeros(3, np.float32)]
+    for P in (2, 4, 8):
+        over = [[np.full(8, 40000.0, np.float16), np.ones(3, np.float16)] for _ in range(P)]
+        G = O.combine([g[0] for g in over], 1.0)
+        assert np.isinf(G).all() and (G > 0).all()
+        r = O.dp_step(kinds, hp(grad_scale=1.0 / P), 100, w, over, m)
+        assert r.skipped and np.array_equal(r.w[0], w[0]) and np.array_equal(r.m[1], m[1])
+        v = np.float16(65504.0 / (2 * P))  # exact: the sum 32752 is far below 65520
+        under = [[np.full(8, v, np.float16), -np.ones(3, np.float16)] for _ in range(P)]
+        assert O.combine([g[0] for g in under], 1.0).tolist() == [32752.0] * 8
+        assert not O.dp_step(kinds, hp(grad_scale=1.0 / P), 100, w, under, m).skipped
+    neg = O.combine([np.array([-65504.0], np.float16), np.array([-16.0], np.float16)], 1.0)
+    assert neg.tolist() == [-np.inf]  # -65520 rounds to -inf (tie to even)
+    assert O.combine([np.array([-65504.0], np.float16), np.array([-15.0], np.float16)], 1.0).tolist() == [-65519.0]
 
 
 def test_dp_step_uses_exact_rank_sum():
