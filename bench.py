@@ -444,6 +444,8 @@ def run_reference(args):
 
 
 def main():
+    # NCCL's own banner ("NCCL version ...") goes to stderr: stdout carries exactly one JSON line
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     args = parse()
     if args.impl == "reference":
         run_reference(args)

@@ -205,6 +205,14 @@ lars_status_t lars_groups(lars_handle_t h, int32_t* ngroups, int64_t* begin, int
  * segments (pieces of layers inside tiles) and warp chunks. Any output may be NULL. */
 lars_status_t lars_work_info(lars_handle_t h, int32_t rank, int32_t* ntiles, int32_t* nsegs, int32_t* nchunks);
 
+/* Verifies the structural invariants of the single-GPU work list (rank < 0) or of a rank's shard that the
+ * kernels rely on for in-bounds, race-free access: tiles partition the segments with no empty tile; a tile's
+ * chunks fit the kernels' shared-memory partials; every tensor's segments tile exactly its elements on this
+ * rank (64-element aligned starts); chunks tile their segment (<= 2,048 elements, 32-byte aligned); nothing
+ * lies outside the rank's shard or the flat buffer. LARS_OK, or LARS_ERR_LAYOUT with *reason (static string,
+ * may be NULL) naming the violated invariant. Host only; no CUDA calls. */
+lars_status_t lars_check_work(lars_handle_t h, int32_t rank, const char** reason);
+
 /* 64-bit FNV-1a hash of (layout, hyper-parameters, P); equal on every rank that planned alike. */
 lars_status_t lars_layout_hash(lars_handle_t h, uint64_t* hash);
 

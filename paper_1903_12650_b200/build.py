@@ -39,16 +39,23 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+CHECKED_LIB = os.path.join(BUILD, "checked", "liblars_b200_checked.so")
+
+
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """checked=True: the diagnostics variant with device-side bounds/invariant checks (-DLARS_DEVICE_CHECKS),
+    written to build/checked/ (never the in-tree product library); load it with LARS_LIB=<path>."""
+    lib = CHECKED_LIB if checked else LIB
+    if not force and not checked and not _stale():
         return LIB
     nccl = nccl_root()
-    os.makedirs(BUILD, exist_ok=True)
+    build_dir = os.path.join(BUILD, "checked") if checked else BUILD
+    os.makedirs(build_dir, exist_ok=True)
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-Wall", "-I", os.path.join(ROOT, "include"),
-              "-I", CSRC, "-I", os.path.join(nccl, "include")]
+              "-I", CSRC, "-I", os.path.join(nccl, "include")] + (["-DLARS_DEVICE_CHECKS"] if checked else [])
     objs = []
     for src in sources():
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        obj = os.path.join(build_dir, os.path.basename(src) + ".o")
         cmd = [NVCC, *ARCH, *common, "-c", src, "-o", obj]
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"]
@@ -58,19 +65,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose and r.stderr:
             print(r.stderr, file=sys.stderr)
         if src.endswith(".cu"):
-            with open(os.path.join(BUILD, "ptxas.log"), "w") as f:
+            with open(os.path.join(build_dir, "ptxas.log"), "w") as f:
                 f.write(r.stderr)
         objs.append(obj)
     libdir = os.path.join(nccl, "lib")
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-L", libdir, "-l:libnccl.so.2",
            "-Xlinker", f"-rpath,{libdir}"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv))

@@ -115,6 +115,8 @@ lars_status_t validate_hparams(const lars_hparams_t& hp);
 lars_status_t make_plan(const lars_tensor_t* t, int32_t n, const lars_hparams_t& hp, Plan& plan);
 // Work list over the tensors owned by `rank` (rank < 0: every tensor), ~ntiles_target tiles.
 WorkList make_worklist(const Plan& plan, int32_t rank, int32_t ntiles_target, int32_t min_tile);
+// nullptr when the work list satisfies every invariant the kernels rely on, else the violated one.
+const char* check_worklist(const Plan& plan, const WorkList& wl, int32_t rank);
 
 // ---- kernel launchers (kernels.cu) ----
 struct DevWork {
@@ -134,6 +136,8 @@ struct DevWork {
   int32_t ntiles;
   int32_t ntensors;
   int32_t grid;      // K1 and K2 CTAs (same grid: CTA b runs on the same SM in both kernels)
+  int32_t nchunks;   // chunks of the work list (device bounds checks)
+  int64_t elem_end;  // flat buffer length (device bounds checks: every chunk lies in [0, elem_end))
 };
 
 struct DevScratch {

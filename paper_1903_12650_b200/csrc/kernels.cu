@@ -24,11 +24,39 @@
 #include <nccl.h>
 #include <nccl_device.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdio>
 
 #include "internal.h"
 
 namespace lars {
+
+// Device-side bounds and invariant checks (tools/checked_build.py builds the library with
+// -DLARS_DEVICE_CHECKS; compute-sanitizer is not available on the GPU pool). Off in the product build.
+#ifdef LARS_DEVICE_CHECKS
+#define LARS_DCHECK(cond)                                                                         \
+  do {                                                                                            \
+    if (!(cond)) {                                                                                \
+      printf("LARS_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__,  \
+             (int)blockIdx.x, (int)threadIdx.x);                                                  \
+      __trap();                                                                                   \
+    }                                                                                             \
+  } while (0)
+#else
+#define LARS_DCHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
+
+// Every access of w, g, m goes through a chunk: it must lie inside the flat buffer, start 32-byte aligned
+// (256-bit vectors) and belong to a local tensor of the work list.
+__device__ __forceinline__ void check_chunk(const DevWork& wk, int32_t c, const Seg& ck) {
+  LARS_DCHECK(c >= 0 && c < wk.nchunks);
+  LARS_DCHECK(ck.begin >= 0 && ck.len > 0 && ck.len <= kChunk && ck.begin + ck.len <= wk.elem_end);
+  LARS_DCHECK((ck.begin & 7) == 0);
+  LARS_DCHECK(ck.tensor >= 0 && ck.tensor < wk.ntensors);
+}
 
 // ---------------------------------------------------------------- 256-bit / 128-bit accessors
 struct F8 { float v[8]; };
@@ -356,6 +384,8 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
   // Phase A: the warps of the CTA stream the tile's chunks independently (no block barrier per layer);
   // chunk partials stay in shared memory.
   const int32_t c0 = wk.tile_chunk[tile], c1 = wk.tile_chunk[tile + 1];
+  LARS_DCHECK(c0 >= 0 && c0 <= c1 && c1 - c0 <= kMaxTileChunks && c1 <= wk.nchunks);
+  LARS_DCHECK(s0 < s1 || wk.ntensors == 0);
   if (carried && tid < c1 - c0) cp_async8(sm_cw + tid, sc.cpart_wnext + c0 + tid);
   if (lane < 2 && s0 + warp < s1) cp_async16((char*)(sm_si + warp) + 16 * lane, (const char*)(wk.seginfo + s0 + warp) + 16 * lane);
   // chunk descriptors are prefetched one iteration ahead (their load would otherwise add a round trip
@@ -363,6 +393,7 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
   Seg nxt = (c0 + warp < c1) ? wk.chunks[c0 + warp] : Seg{0, 0, 0};
   for (int32_t c = c0 + warp; c < c1; c += kWarps) {
     const Seg ck = nxt;
+    check_chunk(wk, c, ck);
     if (c + kWarps < c1) nxt = wk.chunks[c + kWarps];
     const float* wp = w + ck.begin;
     const int64_t gi = ck.begin;  // element index handed to the gradient source
@@ -446,6 +477,9 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
   for (int32_t s = s0 + warp; s < s1; s += kWarps) {
     const SegInfo si = (s == s0 + warp) ? sm_si[warp] : wk.seginfo[s];
     const int32_t a = si.a - c0, b = si.b - c0;
+    LARS_DCHECK(a >= 0 && a < b && b <= c1 - c0);  // the segment's chunk partials are this tile's
+    LARS_DCHECK(si.tensor >= 0 && si.tensor < wk.ntensors && si.nseg >= 1);
+    LARS_DCHECK(si.split < wk.nsplit_total);
     double tw = 0.0, tg = 0.0;
     for (int32_t i = a + lane; i < b; i += 32) {
       tw += sm_cw[i];
@@ -672,6 +706,7 @@ __device__ __forceinline__ void publish_half_tiles(const DevWork& wk, const floa
   for (int32_t tile = blockIdx.x; tile < wk.ntiles; tile += gridDim.x)
     for (int32_t c = wk.tile_chunk[tile] + warp; c < wk.tile_chunk[tile + 1]; c += kWarps) {
       const Seg ck = wk.chunks[c];
+      check_chunk(wk, c, ck);
       const int32_t ng = ck.len >> 3;
       for (int32_t j = lane; j < ng; j += 32) ws.store8(ck.begin + 8 * j, ld8_nc(w + ck.begin + 8 * j));
       for (int32_t i = (ng << 3) + lane; i < ck.len; i += 32) ws.store1(ck.begin + i, w[ck.begin + i]);
@@ -704,6 +739,7 @@ __device__ __forceinline__ void update_chunk(int32_t c, const DevWork& wk, const
   const int lane = threadIdx.x & 31;
   const float s = hy.grad_scale_f, mu = hy.mu;
   const Seg ck = wk.chunks[c];
+  check_chunk(wk, c, ck);
   const float cf = sc.coef[ck.tensor], b = sc.beta[ck.tensor];
   float* wp = w + ck.begin;
   float* mp = m + ck.begin;
@@ -768,6 +804,7 @@ __device__ __forceinline__ void update_item(int32_t item, const DevWork& wk, con
   const int32_t t0 = wk.tile_chunk[tile], tn = wk.tile_chunk[tile + 1] - t0;
   const int32_t c0 = t0 + (int32_t)((int64_t)tn * q / kUpdateSplit);
   const int32_t c1 = t0 + (int32_t)((int64_t)tn * (q + 1) / kUpdateSplit);
+  LARS_DCHECK(tile >= 0 && tile < wk.ntiles && q >= 0 && q < kUpdateSplit && c0 <= c1 && c1 <= wk.nchunks);
   for (int32_t c = c1 - 1 - warp; c >= c0; c -= kWarps)  // backwards: K1's most recent reads first
     update_chunk<DT, CARRY, WS>(c, wk, sc, hy, w, g, g_shift, m, ws);
 }
@@ -939,6 +976,7 @@ __global__ void __launch_bounds__(kThreads, dp_norm_ctas_per_sm(NP)) lars_dp_red
     __syncthreads();
   }
   TRACE_MARK(5)
+  LARS_DCHECK(f.nranks >= 1 && f.nranks <= NP && f.rank >= 0 && f.rank < f.nranks);
   PeerSumGrad<DT, NP> gl;
 #pragma unroll
   for (int p = 0; p < NP; ++p) gl.gp[p] = p < f.nranks ? ncclGetLsaPointer(f.gwin, 0, p) : nullptr;

@@ -57,7 +57,7 @@ T* carve(char*& p, size_t n) {
   return r;
 }
 
-lars_status_t upload(DevBufs& b, int sms, int32_t nsplit_total, bool dp) {
+lars_status_t upload(DevBufs& b, int sms, int32_t nsplit_total, bool dp, int64_t elem_end) {
   const WorkList& wl = b.wl;
   const size_t ns = std::max<size_t>(wl.segs.size(), 1), nt = std::max<size_t>(wl.tensors.size(), 1),
                ntl = wl.tile_seg.size(), nc = std::max<size_t>(wl.chunks.size(), 1);
@@ -121,7 +121,7 @@ lars_status_t upload(DevBufs& b, int sms, int32_t nsplit_total, bool dp) {
     return LARS_ERR_CUDA;
   b.dw = DevWork{seginfo, segs, tile_seg, chunks, tile_chunk, seg_chunk, tsb, tsc, tl, tsplit, split_locals,
                  (int32_t)locals.size(), dp ? nsplit_total : 0, wl.ntiles(), (int32_t)wl.tensors.size(),
-                 std::min<int32_t>(wl.ntiles(), sms * kCtasPerSm)};
+                 std::min<int32_t>(wl.ntiles(), sms * kCtasPerSm), (int32_t)wl.chunks.size(), elem_end};
   (void)sms;
   return LARS_OK;
 }
@@ -383,7 +383,7 @@ lars_status_t lars_init(const lars_tensor_t* tensors, int32_t n, const lars_hpar
       lars_destroy(h);
       return LARS_ERR_CUDA;
     }
-    st = upload(h->full, h->sms, 0, false);
+    st = upload(h->full, h->sms, 0, false, h->plan.padded);
     if (st != LARS_OK) { lars_destroy(h); return st; }
   }
   *out = h;
@@ -505,6 +505,24 @@ lars_status_t lars_work_info(lars_handle_t h, int32_t rank, int32_t* ntiles, int
   if (nsegs) *nsegs = (int32_t)wl->segs.size();
   if (nchunks) *nchunks = (int32_t)wl->chunks.size();
   return LARS_OK;
+}
+
+lars_status_t lars_check_work(lars_handle_t h, int32_t rank, const char** reason) {
+  if (!h || rank >= h->plan.P) return LARS_ERR_INVALID_ARG;
+  WorkList tmp;
+  const WorkList* wl = &h->full.wl;
+  if (rank >= 0) {
+    if (h->shard_ready && rank == h->rank) {
+      wl = &h->shard.wl;
+    } else {
+      const int32_t min_tile = h->hp.tile_elems > 0 ? h->hp.tile_elems : kDefaultMinTile;
+      tmp = make_worklist(h->plan, rank, h->sms * kCtasPerSm, min_tile);
+      wl = &tmp;
+    }
+  }
+  const char* why = check_worklist(h->plan, *wl, rank);
+  if (reason) *reason = why ? why : "ok";
+  return why ? LARS_ERR_LAYOUT : LARS_OK;
 }
 
 lars_status_t lars_layout_hash(lars_handle_t h, uint64_t* hash) {
@@ -642,7 +660,7 @@ lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, cons
     h->ev.resize(2 * (size_t)h->K + 2, nullptr);
     for (auto& e : h->ev) CUDA_OR(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  lars_status_t st = upload(h->shard, h->sms, h->plan.nsplit, true);
+  lars_status_t st = upload(h->shard, h->sms, h->plan.nsplit, true, h->plan.padded);
   if (st != LARS_OK) return st;
   // reduced gradient: the rank's shard, or (groups) a flat buffer whose slices of every group are this rank's
   const size_t red_elems = (size_t)(h->plan.policy == LARS_SHARD_GROUPS ? h->plan.padded : h->plan.S);

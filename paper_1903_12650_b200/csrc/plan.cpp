@@ -349,4 +349,74 @@ static WorkList make_worklist_once(const Plan& p, int32_t rank, int32_t ntiles_t
   return wl;
 }
 
+// Structural invariants every kernel relies on for in-bounds, race-free access (the kernels index w, g, m
+// only through chunks): returns a short reason, or nullptr when the work list is sound.
+//  * tiles partition the segments and every tile holds at least one segment (every CTA that owns a tile
+//    contributes to the step's layer count before the fused path's epoch can advance);
+//  * a tile's chunks fit the shared-memory partial arrays (kMaxTileChunks);
+//  * each local tensor's segments are contiguous, in flat order, and cover exactly the tensor's piece on
+//    this rank; segment starts are 64-element aligned;
+//  * chunks tile their segment, are <= kChunk elements, start 8-element (32 B) aligned and carry the
+//    segment's tensor id;
+//  * every element lies inside the rank's elements (its shard / group slices) and inside the flat buffer.
+const char* check_worklist(const Plan& p, const WorkList& wl, int32_t rank) {
+  const int32_t nt = wl.ntiles(), ns = (int32_t)wl.segs.size(), nc = (int32_t)wl.chunks.size();
+  const int32_t nl = (int32_t)wl.tensors.size();
+  if (nt < 1 || wl.tile_seg.front() != 0 || wl.tile_seg.back() != ns) return "tile_seg does not span the segments";
+  for (int32_t t = 0; t < nt; ++t) {
+    if (ns > 0 && wl.tile_seg[t + 1] <= wl.tile_seg[t]) return "a tile without segments";
+    if (wl.tile_chunk[t] != wl.seg_chunk[wl.tile_seg[t]]) return "tile_chunk inconsistent with seg_chunk";
+    if (wl.tile_chunk[t + 1] - wl.tile_chunk[t] > kMaxTileChunks) return "tile exceeds kMaxTileChunks chunks";
+  }
+  if ((int32_t)wl.seg_chunk.size() != ns + 1 || wl.seg_chunk.front() != 0 || wl.seg_chunk.back() != nc)
+    return "seg_chunk does not span the chunks";
+  if ((int32_t)wl.tseg_begin.size() != nl || (int32_t)wl.tseg_count.size() != nl || (int32_t)wl.tlars.size() != nl ||
+      (int32_t)wl.tsplit.size() != nl)
+    return "per-tensor tables have the wrong length";
+  int64_t elems = 0;
+  int32_t next_seg = 0;
+  for (int32_t li = 0; li < nl; ++li) {
+    const int32_t l = wl.tensors[li];
+    if (l < 0 || l >= p.L) return "tensor id out of range";
+    if (li && p.offset[wl.tensors[li - 1]] >= p.offset[l]) return "tensors not in flat order";
+    if (wl.tlars[li] != (p.kind[l] == LARS_KIND_WEIGHT ? 1 : 0)) return "tlars differs from the tensor kind";
+    int64_t lo, hi;
+    piece(p, l, rank, lo, hi);
+    if (hi <= lo) return "a listed tensor has no elements here";
+    if (rank >= 0 && (wl.tsplit[li] >= 0) != (p.split[l] >= 0)) return "tsplit differs from the plan";
+    if (wl.tseg_begin[li] != next_seg || wl.tseg_count[li] < 1) return "tensor segments not contiguous";
+    int64_t pos = p.offset[l] + lo;
+    for (int32_t s = wl.tseg_begin[li]; s < wl.tseg_begin[li] + wl.tseg_count[li]; ++s) {
+      const Seg& sg = wl.segs[s];
+      if (sg.tensor != li || sg.begin != pos || sg.len <= 0) return "segments do not tile the tensor piece";
+      if (sg.begin % kAlign) return "segment start not 64-element aligned";
+      int64_t cpos = sg.begin;
+      for (int32_t c = wl.seg_chunk[s]; c < wl.seg_chunk[s + 1]; ++c) {
+        const Seg& ck = wl.chunks[c];
+        if (ck.tensor != li || ck.begin != cpos || ck.len <= 0 || ck.len > kChunk) return "chunks do not tile the segment";
+        if (ck.begin % 8) return "chunk start not 32-byte aligned";
+        cpos += ck.len;
+      }
+      if (cpos != sg.begin + sg.len) return "chunks do not cover the segment";
+      pos += sg.len;
+    }
+    if (pos != p.offset[l] + hi) return "segments do not cover the tensor piece";
+    if (p.offset[l] + hi > p.padded) return "elements beyond the flat buffer";
+    if (rank >= 0) {  // inside the rank's elements
+      int64_t b = (int64_t)rank * p.S, e = b + p.S;
+      if (p.policy == LARS_SHARD_GROUPS) {
+        const Plan::Group& g = p.groups[p.group_of[l]];
+        b = g.begin + rank * (g.len / p.P);
+        e = b + g.len / p.P;
+      }
+      if (p.offset[l] + lo < b || p.offset[l] + hi > e) return "elements outside the rank's shard";
+    }
+    elems += hi - lo;
+    next_seg += wl.tseg_count[li];
+  }
+  if (next_seg != ns) return "segments not owned by any tensor";
+  if (elems != wl.elems) return "element count differs";
+  return nullptr;
+}
+
 }  // namespace lars

@@ -56,11 +56,14 @@ class HParams(ctypes.Structure):
 _lib = None
 
 
-def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
-    """Loads the in-tree library (built by ``__graft_entry__.build()``). Fails loudly if absent."""
+def load_library(path: str | None = None) -> ctypes.CDLL:
+    """Loads the in-tree library (built by ``__graft_entry__.build()``). Fails loudly if absent.
+    LARS_LIB=<path> selects another build of the same library (the device-checked diagnostics variant,
+    ``python -m paper_1903_12650_b200.build --checked``)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("LARS_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise LarsLibraryMissing(f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
     lib = ctypes.CDLL(path)
@@ -74,6 +77,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "lars_shard_range": (c_int32, [h, c_int32, POINTER(c_int64), POINTER(c_int64)]),
         "lars_tensor_owner": (c_int32, [h, POINTER(c_int32)]),
         "lars_layout_hash": (c_int32, [h, POINTER(c_uint64)]),
+        "lars_check_work": (c_int32, [h, c_int32, POINTER(ctypes.c_char_p)]),
         "lars_init_weights": (c_int32, [h, c_void_p, ctypes.c_uint64, c_void_p]),
         "lars_work_info": (c_int32, [h, c_int32, POINTER(c_int32), POINTER(c_int32), POINTER(c_int32)]),
         "lars_step": (c_int32, [h, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
@@ -248,6 +252,14 @@ class Lars:
         t, sg, c = c_int32(), c_int32(), c_int32()
         _check(self._lib.lars_work_info(self._h, rank, byref(t), byref(sg), byref(c)), "lars_work_info")
         return {"tiles": t.value, "segments": sg.value, "chunks": c.value}
+
+    def check_work(self, rank: int = -1) -> str:
+        """Structural invariants of a work list (lars_check_work): 'ok', or raises LarsError with the reason."""
+        why = ctypes.c_char_p()
+        st = self._lib.lars_check_work(self._h, rank, byref(why))
+        if st != 0:
+            raise LarsError(st, f"lars_check_work: {why.value.decode() if why.value else '?'}")
+        return why.value.decode()
 
     def layout_hash(self) -> int:
         x = c_uint64()
