@@ -61,6 +61,56 @@ def workload_name(P: int, layout: str) -> str:
     return f"{layout}_f32_lars_step_1gpu" if P == 1 else f"{layout}_f16_rs_lars_ag_dp{P}"
 
 
+def workload_config(P: int, layout: str, lay) -> dict:
+    """The workload both arms report (identical dict for `--impl ours` and `--impl reference`)."""
+    E = sum(t.numel for t in lay)
+    gbytes = 4 if P == 1 else 2
+    return {"workload": workload_name(P, layout), "layout": layout, "tensors": len(lay), "params": E,
+            "grad_dtype": "f32" if P == 1 else "f16", "global_batch": HP["global_batch"],
+            "iters": f"t=({T0}+k) mod 1440", "parallelism": f"dp{P}",
+            "units": f"{P} x {E} gradient params combined+applied per step",
+            "l2": f"inputs larger than L2: w+g+m = {(8 + gbytes) * E / 1e6:.0f} MB > 126 MB, no flush"}
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class OneCore:
+    """Runs the oracle on exactly one host core: the calling thread pinned to one CPU of its affinity set
+    and BLAS/OpenMP pools limited to one thread (the oracle's NumPy ufuncs and math.fsum are single-threaded
+    anyway); the previous affinity is restored on exit."""
+
+    def __enter__(self):
+        self.prev = os.sched_getaffinity(0)
+        self.core = max(self.prev)  # away from core 0 (interrupts, the GPU driver's threads)
+        os.sched_setaffinity(0, {self.core})
+        self.pool = None
+        try:
+            from threadpoolctl import threadpool_limits
+
+            self.pool = threadpool_limits(1)
+        except ImportError:
+            pass
+        return self
+
+    def __exit__(self, *exc):
+        if self.pool is not None:
+            self.pool.restore_original_limits()
+        os.sched_setaffinity(0, self.prev)
+        return False
+
+    def describe(self) -> str:
+        return f"pinned to CPU {self.core} of {len(self.prev)} ({cpu_model()})"
+
+
 def measured_peaks() -> dict:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -192,13 +242,24 @@ def run_ours(args):
     while time.time() < t_end:
         run(20)
         torch.cuda.synchronize()
+    nvl = None
+    if P > 1:  # NVLink hardware byte counters around the timed steps (ncu cannot replay cross-rank kernels)
+        try:
+            from tools.nvlink_counters import NvlinkCounters
+
+            nvl = NvlinkCounters(local)
+            nvl = nvl if nvl.available() else None
+        except Exception:  # noqa: BLE001 - counters are evidence, not part of the step
+            nvl = None
     barrier()
     torch.cuda.synchronize()
+    nvl0 = nvl.read() if nvl else None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     run(args.steps)
     e1.record(stream)
     torch.cuda.synchronize()
+    nvl1 = nvl.read() if nvl else None
     barrier()
     clk = clocks.stop()
     ms_total = max_over_ranks(e0.elapsed_time(e1))
@@ -334,6 +395,14 @@ def run_ours(args):
                 "step_frac_of_bus_roofline": round(bus / NVLINK_PEER_GBS / 1e9 / (ms_step * 1e-3), 4),
                 # north_star framing: 900 GB/s per direction nominal NVLink 5 beside the measured peer copy
                 "frac_of_nominal": round(ach / NVLINK_NOMINAL_GBS, 4), "nominal_peak": NVLINK_NOMINAL_GBS}
+    if nvl0 and nvl1:  # this rank's link payload per step vs the algorithmic bus bytes (RS in + AG out)
+        roof["nvlink_counters"] = {
+            "tx_bytes_per_step": int((nvl1["tx"] - nvl0["tx"]) / args.steps),
+            "rx_bytes_per_step": int((nvl1["rx"] - nvl0["rx"]) / args.steps),
+            # each direction of a GPU's links carries (P-1)/P * (gbytes + 4) * N per step: the shard pulls
+            # (RS) and the weight stores (AG) leave on one direction and arrive on the other
+            "algorithmic_bytes_per_direction": int(bus),
+            "source": nvl.describe()}
     step_alg = (upd_bytes) / (ms_step * 1e-3) / 1e9
     two_pass = upd_bytes + (gbytes if carry else 4 + gbytes) * shard_elems
     out = {
@@ -341,13 +410,9 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "grad_dtype": dtype, "data": "synthetic",
         "carry_wnorm": carry, **alt,
-        "config": {"workload": workload_name(P, args.layout), "layout": args.layout, "tensors": len(lay),
-                   "params": E, "global_batch": HP["global_batch"], "iters": f"t=({T0}+k) mod {T}",
-                   "parallelism": f"dp{P}", "units": f"{P} x {E} gradient params combined+applied per step",
-                   "dp_path": None if P == 1 else ("fused-nvlink" if fused else "nccl"),
-                   "nccl_buckets": args.buckets if P > 1 else None,
-                   "l2": f"inputs larger than L2: w+g+m = {(8 + gbytes) * h.padded_numel / 1e6:.0f} MB > 126 MB, "
-                         "no flush"},
+        "config": workload_config(P, args.layout, lay),
+        "dp_path": None if P == 1 else ("fused-nvlink" if fused else "nccl"),
+        "nccl_buckets": args.buckets if P > 1 else None,
         "phases_ms": {kk: round(v, 5) for kk, v in ph.items() if v > 0},
         "roofline": roof,
         "roofline_step": ({"bound": "hbm", "achieved": round(step_alg, 1), "peak": hbm, "unit": "GB/s",
@@ -383,13 +448,15 @@ def cpu_baseline(lay, w, g_ranks, m, dtype, P):
 
     hp = O.HParams(grad_scale=1.0 / (G.GRAD_PRESCALE * P), **HP)
     kinds = [t.kind for t in lay]
-    t0 = time.perf_counter()
-    O.step(kinds, hp, T0, w, g_ranks, m)
-    dt = time.perf_counter() - t0
+    with OneCore() as oc:
+        t0 = time.perf_counter()
+        O.step(kinds, hp, T0, w, g_ranks, m)
+        dt = time.perf_counter() - t0
     E = sum(t.numel for t in lay)
     return {"value": round(P * E / dt, 1), "unit": "params/s", "cores": 1, "kind": "oracle",
+            "cpu": cpu_model(),
             "sample": f"1 full {len(lay)}-tensor step ({E} params, {dtype} grads) in {dt:.2f} s, "
-                      f"single-threaded NumPy float64 + math.fsum"}
+                      f"NumPy float64 + math.fsum, {oc.describe()}"}
 
 
 # ----------------------------------------------------------------------------------------- reference
@@ -405,6 +472,7 @@ def run_reference(args):
     lay = LY.by_name(args.layout)
     E = sum(t.numel for t in lay)
     hp = O.HParams(grad_scale=1.0 / (G.GRAD_PRESCALE * P), **HP)
+    oc = OneCore().__enter__()  # the whole reference arm runs on one host core
     # calibrate on the first few tensors, then size a contiguous tensor prefix so the whole run is bounded
     cal = lay[:40]
     wc, gc, mc = G.weights(cal), [G.grads(cal, r, 0, dtype) for r in range(P)], G.momentum(cal, 1e-3)
@@ -429,16 +497,14 @@ def run_reference(args):
     dt = time.perf_counter() - t0
     value = P * acc * args.steps / dt
     sample = (f"first {n} of {len(lay)} tensors ({acc} of {E} params), {P} rank gradient(s) of {dtype}, "
-              f"per step; single-threaded NumPy float64 + math.fsum")
+              f"per step; NumPy float64 + math.fsum, {oc.describe()}")
     out = {"impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": "params/s", "n_gpus": P,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "grad_dtype": dtype,
            "data": "synthetic",
-           "config": {"workload": workload_name(P, args.layout), "layout": args.layout, "tensors": len(lay),
-                      "params": E, "global_batch": HP["global_batch"], "parallelism": f"dp{P}",
-                      "units": f"{P} x sampled params per step"},
+           "config": workload_config(P, args.layout, lay),
            "cpu_baseline": {"value": round(value, 1), "unit": "params/s", "cores": 1, "kind": "oracle",
-                            "sample": sample},
+                            "cpu": cpu_model(), "sample": sample},
            "e2e": {"value": round(value, 1), "unit": "params/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 

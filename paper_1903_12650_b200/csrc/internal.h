@@ -172,6 +172,8 @@ struct Hyper {
   bool carry;                // LARS_FLAG_CARRY_WNORM
   bool lr_at_apply;          // LARS_FLAG_LR_AT_APPLY (SPEC.md:186 momentum form)
   void* w_half = nullptr;    // LARS_FLAG_HALF_WEIGHTS: compute weights (grad dtype) the update also writes
+  int32_t k2_prefetch = 0;   // K2: chunks per CTA whose w, m are prefetched into L2 before its PDL wait
+  bool k2_prefetch_g = false;  // ... and their gradient
 };
 
 // g_shift: the gradient of flat element e is g[e - g_shift] (the DP step reads its reduced shard).

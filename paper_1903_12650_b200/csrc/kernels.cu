@@ -111,6 +111,20 @@ __device__ __forceinline__ uint4 ld16_nc(const void* p) {
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
+// read-only, keep in L2 for K2 (the .L2::evict_last qualifier takes 256-bit vectors only; a 128-bit load
+// carries the same priority as an L2 cache-hint policy)
+__device__ __forceinline__ uint4 ld16_keep(const void* p) {
+  uint4 r;
+  asm("{\n\t.reg .b64 pol;\n\t"
+      "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+      "ld.global.nc.L1::no_allocate.L2::cache_hint.v4.b32 {%0,%1,%2,%3}, [%4], pol;\n\t}"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+// L2 prefetch of a contiguous range by the bulk-copy engine (no registers held; 16 B aligned, 16 B multiple)
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 
 // Gradient access by wire dtype. Widening fp16/bf16 -> fp32 is exact.
 template <int DT> struct Grad;
@@ -147,14 +161,14 @@ __device__ __forceinline__ F8 widen_b8(uint4 r) {
   return o;
 }
 template <> struct Grad<LARS_F16> {
-  __device__ __forceinline__ static F8 load8_keep(const void* g, int64_t i) { return widen_h8(ld16_nc((const __half*)g + i)); }
+  __device__ __forceinline__ static F8 load8_keep(const void* g, int64_t i) { return widen_h8(ld16_keep((const __half*)g + i)); }
   __device__ __forceinline__ static F8 load8(const void* g, int64_t i) { return widen_h8(ld16_nc((const __half*)g + i)); }
   __device__ __forceinline__ static float load1(const void* g, int64_t i) { return __half2float(((const __half*)g)[i]); }
   __device__ __forceinline__ static uint4 raw8(const void* g, int64_t i) { return ld16_nc((const __half*)g + i); }
   __device__ __forceinline__ static F8 widen(const uint4& r) { return widen_h8(r); }
 };
 template <> struct Grad<LARS_BF16> {
-  __device__ __forceinline__ static F8 load8_keep(const void* g, int64_t i) { return widen_b8(ld16_nc((const uint16_t*)g + i)); }
+  __device__ __forceinline__ static F8 load8_keep(const void* g, int64_t i) { return widen_b8(ld16_keep((const uint16_t*)g + i)); }
   __device__ __forceinline__ static F8 load8(const void* g, int64_t i) { return widen_b8(ld16_nc((const uint16_t*)g + i)); }
   __device__ __forceinline__ static float load1(const void* g, int64_t i) {
     return __uint_as_float((uint32_t)((const uint16_t*)g)[i] << 16);
@@ -594,8 +608,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_norms_kernel(DevWor
                                                                           const float* __restrict__ w,
                                                                           const void* __restrict__ g,
                                                                           int64_t g_shift) {
-  pdl_trigger();
+  // wait BEFORE releasing the dependent K2: K2 prefetches w and m before its own wait, so it must not
+  // become resident while the previous step's K2 may still be writing them
   pdl_wait();
+  pdl_trigger();
   TRACE_BEGIN
   norms_body<CARRY>(wk, sc, hy, w, LocalGrad<DT>{g, g_shift});
   TRACE_END(0)
@@ -809,6 +825,30 @@ __device__ __forceinline__ void update_item(int32_t item, const DevWork& wk, con
     update_chunk<DT, CARRY, WS>(c, wk, sc, hy, w, g, g_shift, m, ws);
 }
 
+// Before K2's griddepcontrol.wait (its CTAs become resident as K1's retire): the bulk-copy engine
+// prefetches into L2 the w and m (and optionally g) of the first hy.k2_prefetch chunks this CTA will
+// update — the last chunks of its tile's last part (update_item's order) — so the HBM that K1's
+// layer-finishing tail leaves idle already streams K2's first bytes. Safe: K1 triggered this launch only
+// after its own wait, i.e. after the previous step's K2 completed.
+template <int DT>
+__device__ __forceinline__ void k2_prefetch_first(const DevWork& wk, const Hyper& hy, const float* w, const void* g,
+                                                  int64_t g_shift, const float* m) {
+  const int32_t tile = blockIdx.x;
+  if (tile >= wk.ntiles) return;
+  const int32_t t0 = wk.tile_chunk[tile], tn = wk.tile_chunk[tile + 1] - t0;
+  const int32_t c0 = t0 + (int32_t)((int64_t)tn * (kUpdateSplit - 1) / kUpdateSplit), c1 = t0 + tn;
+  constexpr int kEs = DT == LARS_F32 ? 4 : 2;
+  for (int32_t i = threadIdx.x; i < hy.k2_prefetch && c1 - 1 - i >= c0; i += blockDim.x) {
+    const Seg ck = wk.chunks[c1 - 1 - i];
+    const uint32_t wb = ((uint32_t)ck.len * 4u) & ~15u, gb = ((uint32_t)ck.len * kEs) & ~15u;
+    if (wb) {
+      prefetch_l2_bulk(w + ck.begin, wb);
+      prefetch_l2_bulk(m + ck.begin, wb);
+    }
+    if (hy.k2_prefetch_g && gb) prefetch_l2_bulk((const char*)g + (ck.begin - g_shift) * kEs, gb);
+  }
+}
+
 // K2. Same persistent schedule as K1 (CTA b owns tiles b, b + grid, ...; identical grid and resources,
 // so CTA b runs on the same SM in both kernels) and each tile's chunks walked backwards: the gradient
 // bytes K1 streamed last into this SM's L2 slice are re-read first.
@@ -818,6 +858,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_update_kernel(DevWo
                                                                            const void* __restrict__ g,
                                                                            int64_t g_shift, float* __restrict__ m) {
   pdl_trigger();
+  // K1 writes none of w, g, m: while K1 drains, pull the first chunks this CTA updates into L2
+  if (hy.k2_prefetch > 0) k2_prefetch_first<DT>(wk, hy, w, g, g_shift, m);
   pdl_wait();
   const bool skip = *(volatile const int32_t*)sc.skip != 0;  // whole step skipped (non-finite norm)
   TRACE_BEGIN
@@ -957,7 +999,11 @@ __global__ void __launch_bounds__(kThreads, dp_norm_ctas_per_sm(NP)) lars_dp_red
   pdl_wait();
   // Entry: every rank's gradient for this step is complete once every rank's F1 is running. CTA 0 alone
   // syncs with the other ranks (one LSA barrier instead of one per CTA); the others wait for its go flag.
-  // The step epoch cannot move during the entry: the CTA that advances it is the last to finish a tile.
+  // The step epoch cannot move during the entry: it is advanced by the CTA that completes the layer
+  // count, which needs every tile-owning CTA past its entry. A CTA that owns no tile (the launcher caps
+  // the grid at one CTA per tile; this guards any other grid) leaves before reading the epoch: it could
+  // otherwise read the NEXT epoch and wait for a go flag that never comes.
+  if (blockIdx.x != 0 && (int32_t)blockIdx.x >= wk.ntiles) return;
   {
     const unsigned long long E = *(volatile const unsigned long long*)f.epoch;
     if (blockIdx.x == 0) {
@@ -1111,6 +1157,7 @@ cudaError_t launch_dp_fused(int32_t dt, const DevWork& wk, const DevScratch& sc,
                             const DpFused& f, int grid_norm, int grid_update, cudaStream_t st, cudaEvent_t ev1,
                             cudaEvent_t ev2) {
   DevWork wg = wk;
+  grid_norm = std::min(grid_norm, std::max(wk.ntiles, 1));  // one CTA per tile (F1's entry relies on it)
   wg.grid = grid_norm;
   launch_reduce_norms(dt, hy.carry, f.np_template, grid_norm, st, wg, sc, hy, w, f);
   if (ev1) cudaEventRecord(ev1, st);

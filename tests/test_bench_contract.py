@@ -36,9 +36,20 @@ def _check_base(d):
         assert k in d["e2e"], k
 
 
+def _same_config_as_cuda_arm(d):
+    """Both arms report the identical workload dict (the driver compares them)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from synth import layouts as LY
+
+    assert d["config"] == bench.workload_config(d["n_gpus"], "resnet50", LY.by_name("resnet50"))
+
+
 def test_reference_arm_line():
     d = _line(["--impl", "reference", "--steps", "1", "--warmup", "0"])
     _check_base(d)
+    _same_config_as_cuda_arm(d)
+    assert "pinned to CPU" in d["cpu_baseline"]["sample"] and d["cpu_baseline"]["cpu"]
     assert d["impl"] == "reference" and d["dtype"] == "f64"
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
@@ -49,6 +60,7 @@ def test_reference_arm_line():
 def test_cuda_arm_line():
     d = _line(["--steps", "5", "--warmup", "3", "--soak-s", "0", "--e2e-steps", "1"])
     _check_base(d)
+    _same_config_as_cuda_arm(d)
     roof = d["roofline"]
     for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
         assert k in roof, k
