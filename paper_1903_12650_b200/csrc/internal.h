@@ -41,6 +41,8 @@ constexpr int32_t kMaxTileChunks = 256; // chunk partials of one tile live in sh
 constexpr int32_t kUpdateSplit = 4;     // K2 walks each tile in 4 parts, last part first
 constexpr int kNormUnroll = LARS_NORM_UNROLL;  // K1 vector groups per lane per iteration
 constexpr int32_t kDefaultMinTile = 4096;
+constexpr bool kK1BulkDefault = false;  // K1 bulk-copy streaming (Hyper::k1_bulk) unless LARS_K1_BULK says
+constexpr bool kDpBulkDefault = false;  // F1 bulk-copy streaming (DpFused::bulk) unless LARS_DP_BULK says
 constexpr int32_t kChunk = 2048;        // elements per warp work item (multiple of 256)
 
 // One contiguous piece of one tensor inside one work tile. begin is a flat element offset,
@@ -174,6 +176,7 @@ struct Hyper {
   void* w_half = nullptr;    // LARS_FLAG_HALF_WEIGHTS: compute weights (grad dtype) the update also writes
   int32_t k2_prefetch = 0;   // K2: chunks per CTA whose w, m are prefetched into L2 before its PDL wait
   bool k2_prefetch_g = false;  // ... and their gradient
+  bool k1_bulk = false;      // K1 streams its chunks through the bulk-copy engine (stream_tile_bulk)
 };
 
 // g_shift: the gradient of flat element e is g[e - g_shift] (the DP step reads its reduced shard).
@@ -195,11 +198,14 @@ struct DpFused {
   bool mcast;                     // NVLS multicast all-gather (multimem.st) instead of per-peer stores
   int np_template;                // F1 peer-count template bound (>= nranks; 2, 4 or 8)
   ncclWindow_t hwin = nullptr;    // LARS_FLAG_HALF_WEIGHTS: compute-weight window (grad dtype), else null
+  bool bulk = false;              // F1 streams the rank sum through bulk-copy stages (TMA peer reads)
 };
 // F1 (reduce + norms + share publication, grid_norm CTAs), then F2 (share collection + update + gather,
 // grid_update CTAs, programmatic dependent launch). Events (optional, profiling) are recorded after F1.
 // Resident CTAs per SM of the F1 instance (grad dtype, carry, peer-count template) that will be launched.
-int dp_reduce_norms_blocks_per_sm(int32_t grad_dtype, bool carry, int np_template);
+int dp_reduce_norms_blocks_per_sm(int32_t grad_dtype, bool carry, int np_template, bool bulk);
+// Resident K1 CTAs per SM when K1 streams through bulk-copy stages (Hyper::k1_bulk).
+int norms_bulk_blocks_per_sm(int32_t grad_dtype, bool carry);
 // Compute weights (grad dtype) of every element of the work list = RNE(w) (LARS_FLAG_HALF_WEIGHTS).
 cudaError_t launch_publish_half(int32_t grad_dtype, const DevWork& wk, const float* w, void* w_half, cudaStream_t stream);
 cudaError_t launch_dp_fused(int32_t grad_dtype, const DevWork& wk, const DevScratch& sc, const Hyper& hy, float* w,

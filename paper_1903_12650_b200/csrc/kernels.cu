@@ -214,6 +214,13 @@ extern "C" int lars_trace_arm(void* buf) {
 // Plain: the (already combined) gradient in local memory; element e lives at g[e - shift].
 template <int DT>
 struct LocalGrad {
+  static constexpr bool kBulk = true;  // may stream through the bulk-copy engine (stream_tile_bulk)
+  static constexpr int kDt = DT;
+  static constexpr int kPeers = 0;
+  __device__ __forceinline__ int nsrc() const { return 1; }
+  __device__ __forceinline__ const void* src(int, int64_t e) const {
+    return (const char*)g + (e - shift) * (DT == LARS_F32 ? 4 : 2);
+  }
   static constexpr int kUnroll = kNormUnroll;  // (w, g) groups per lane per iteration
   static constexpr int kUnrollG = LARS_NORM_UNROLL_G;  // g-only groups per lane per iteration (carried norms)
   const void* g;
@@ -244,6 +251,9 @@ __device__ __forceinline__ float wire_saturate(float x) {
 constexpr int kMaxRanks = 8;
 template <int DT, int NP>  // NP: compile-time upper bound of the rank count (2, 4 or 8)
 struct PeerSumGrad {
+  static constexpr bool kBulk = true;
+  static constexpr int kDt = DT;
+  static constexpr int kPeers = NP;
   const void* gp[NP];         // gradient buffer of every rank (index = rank < nranks), same flat layout
   int nranks;
   float* gred;                // local fp32 reduced shard: element e at gred[e - begin]
@@ -275,6 +285,11 @@ struct PeerSumGrad {
     return acc;
   }
   __device__ __forceinline__ F8 load8(int64_t e, bool) const { return load8(e); }
+  __device__ __forceinline__ int nsrc() const { return nranks; }
+  __device__ __forceinline__ const void* src(int p, int64_t e) const {
+    return (const char*)gp[p] + e * (DT == LARS_F32 ? 4 : 2);
+  }
+  __device__ __forceinline__ void store8(int64_t e, const F8& x) const { st8_noclobber(gred + (e - begin), x); }
   __device__ __forceinline__ float load1(int64_t e) const {
     float acc = 0.f;
     for (int p = 0; p < nranks; ++p) acc += Grad<DT>::load1(gp[p], e);
@@ -295,6 +310,36 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// ---------------------------------------------------------------- bulk copies (TMA engine) + mbarriers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  } while (!ok);
+}
+// order this thread's earlier generic-proxy accesses of shared memory before later async-proxy (bulk copy) ones
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// global -> shared bulk copy by the TMA engine; completes `bytes` of transaction count on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
+}
+
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
@@ -302,11 +347,11 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // drains and must call pdl_wait() before touching anything the predecessor writes. coop: cooperative
 // launch — the driver guarantees every CTA of the grid is co-resident (F1's CTAs wait on CTA 0's flag).
 template <typename K, typename... Args>
-static cudaError_t launch_pdl_ex(K kernel, int grid, cudaStream_t stream, bool coop, Args... args) {
+static cudaError_t launch_pdl_smem(K kernel, int grid, cudaStream_t stream, bool coop, size_t smem, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -318,13 +363,26 @@ static cudaError_t launch_pdl_ex(K kernel, int grid, cudaStream_t stream, bool c
   return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 template <typename K, typename... Args>
+static cudaError_t launch_pdl_ex(K kernel, int grid, cudaStream_t stream, bool coop, Args... args) {
+  return launch_pdl_smem(kernel, grid, stream, coop, 0, args...);
+}
+template <typename K, typename... Args>
 static cudaError_t launch_pdl(K kernel, int grid, cudaStream_t stream, Args... args) {
   return launch_pdl_ex(kernel, grid, stream, false, args...);
 }
 
+// Sum of squares added to a fp64 accumulator: exact fp64 squares of the fp32 values, fp64 adds (reading #15).
+// (Summing each 8-element group in fp32 and widening once, with an fp64 redo for out-of-range groups, was
+// measured: -1 us on fp32/fp16 gradients, +5 us on bf16 — the conversions are not what bounds K1. Not kept.)
 __device__ __forceinline__ void acc8(double& a, const F8& x) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) a = fma((double)x.v[i], (double)x.v[i], a);
+}
+__device__ __forceinline__ void acc4(double& a, const float4& x) {
+  a = fma((double)x.x, (double)x.x, a);
+  a = fma((double)x.y, (double)x.y, a);
+  a = fma((double)x.z, (double)x.z, a);
+  a = fma((double)x.w, (double)x.w, a);
 }
 
 // ---------------------------------------------------------------- K1: segmented norms + finish
@@ -382,11 +440,143 @@ __device__ __forceinline__ bool finish_core(int32_t l, double sw, double sg, con
   return finish_core(l, wk.tlars[l], sw, sg, sc, hy, step_lr(hy));
 }
 
+// K1 phase A through the bulk-copy engine (single GPU / NCCL path, hy.k1_bulk): every warp streams its
+// chunks (c0 + warp, c0 + warp + 8, ...) as pieces of <= 2 KB (pe elements of g, plus w when the weight
+// norms are not carried) through kBulkStages private shared-memory stages. Lane 0 keeps kBulkStages pieces in
+// flight with cp.async.bulk (no registers held per byte in flight, unlike the register loop, whose loads in
+// flight per lane are capped by the 64-register budget); each stage has an mbarrier completed by the copy's
+// transaction count. The warp sums squares from shared memory in fp64 (fixed order: lane, piece, then the
+// xor butterfly), the < 8 ragged elements at a tensor's end straight from global memory. Gradient and
+// weight bytes are fetched with an L2 evict_last policy (K2 re-reads them).
+constexpr int kBulkStages = 3;                 // per warp
+constexpr int kBulkStageBytes = 2048;
+constexpr int kBulkSmem = kThreads / 32 * kBulkStages * kBulkStageBytes;  // 48 KB dynamic shared memory
+
+// GL: LocalGrad<DT> (K1: one gradient source) or PeerSumGrad<DT, NP> (F1: the gradient of every rank, read
+// over NVLink from the symmetric window; the consumer sums the ranks in order in fp32, applies the wire
+// saturation, stores the sum into the fp32 reduced shard and accumulates its square).
 template <class GL>
+__device__ __forceinline__ void stream_tile_bulk(int32_t c0, int32_t c1, const DevWork& wk, const float* __restrict__ w,
+                                                 const GL& gl, bool carried, double* sm_cw, double* sm_cg,
+                                                 unsigned char* stages, uint64_t* bars, uint32_t& q) {
+  constexpr int DT = GL::kDt;
+  constexpr int kEs = DT == LARS_F32 ? 4 : 2;
+  constexpr int kWarps = kThreads / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nsrc = gl.nsrc();
+  const int32_t cw0 = c0 + warp;
+  const int32_t nk = cw0 < c1 ? (c1 - cw0 + kWarps - 1) / kWarps : 0;  // this warp's chunks (<= 32)
+  LARS_DCHECK(nk <= 32);
+  // lane k holds the descriptor of this warp's k-th chunk (shuffled to the whole warp when needed)
+  const Seg my = lane < nk ? wk.chunks[cw0 + kWarps * lane] : Seg{0, 0, 0};
+  // piece elements: one stage holds w (unless carried) and every source's gradient for pe elements
+  const int32_t pe = kBulkStageBytes / (nsrc * kEs + (carried ? 0 : 4)) / 8 * 8;
+  const int32_t goff = carried ? 0 : pe * 4;  // gradient sub-buffers start here, pe * kEs bytes each
+  const uint64_t pol = l2_policy_evict_last();
+  unsigned char* wst = stages + warp * kBulkStages * kBulkStageBytes;
+  uint64_t* wbar = bars + warp * kBulkStages;
+  int32_t pk = 0, pj = 0;  // producer cursor: chunk pk, element pj inside it
+  uint32_t pq = q;         // next piece to produce (piece q lives in stage q % kBulkStages)
+  auto produce = [&]() {   // warp-uniform; lane 0 issues
+    if (pk >= nk) return;
+    const int64_t begin = __shfl_sync(0xffffffffu, my.begin, pk);
+    const int32_t len = __shfl_sync(0xffffffffu, my.len, pk);
+    const int32_t n = min(pe, len - pj), nb = n & ~7;
+    if (lane == 0) {
+      const uint32_t st = pq % kBulkStages;
+      unsigned char* dst = wst + st * kBulkStageBytes;
+      fence_proxy_async_smem();  // this warp's reads of the stage's previous piece precede the copy
+      mbar_arrive_expect_tx(wbar + st, (uint32_t)nb * (nsrc * kEs + (carried ? 0 : 4)));
+      if (nb > 0) {
+        const int64_t e = begin + pj;
+        if (!carried) bulk_g2s(dst, w + e, (uint32_t)nb * 4u, wbar + st, pol);
+        for (int p = 0; p < nsrc; ++p)
+          bulk_g2s(dst + goff + p * pe * kEs, gl.src(p, e), (uint32_t)nb * kEs, wbar + st, pol);
+      }
+    }
+    ++pq;
+    pj += pe;
+    if (pj >= len) {
+      pj = 0;
+      ++pk;
+    }
+  };
+#pragma unroll
+  for (int i = 0; i < kBulkStages; ++i) produce();
+  for (int32_t k = 0; k < nk; ++k) {
+    const int64_t begin = __shfl_sync(0xffffffffu, my.begin, k);
+    const int32_t len = __shfl_sync(0xffffffffu, my.len, k);
+    double aw = 0.0, ag = 0.0;
+    for (int32_t j = 0; j < len; j += pe) {
+      const uint32_t st = q % kBulkStages;
+      mbar_wait(wbar + st, (q / kBulkStages) & 1u);
+      const int32_t n = min(pe, len - j), nb = n & ~7;
+      const unsigned char* src = wst + st * kBulkStageBytes;
+      if (!carried)
+        for (int32_t i = 4 * lane; i < nb; i += 128) {
+          acc4(aw, *reinterpret_cast<const float4*>(src + 4 * i));
+        }
+      if constexpr (GL::kPeers == 0) {
+        const unsigned char* gs = src + goff;
+        if constexpr (DT == LARS_F32) {
+          for (int32_t i = 4 * lane; i < nb; i += 128) {
+            acc4(ag, *reinterpret_cast<const float4*>(gs + 4 * i));
+          }
+        } else {
+          for (int32_t i = 8 * lane; i < nb; i += 256) acc8(ag, Grad<DT>::widen(*reinterpret_cast<const uint4*>(gs + 2 * i)));
+        }
+      } else {  // rank sum (rank order, fp32) of 8-element groups, stored to the reduced shard
+        for (int32_t i = 8 * lane; i < nb; i += 256) {
+          F8 acc;
+#pragma unroll
+          for (int t = 0; t < 8; ++t) acc.v[t] = 0.f;
+          for (int p = 0; p < nsrc; ++p) {
+            const unsigned char* gs = src + goff + p * pe * kEs + i * kEs;
+            F8 x;
+            if constexpr (DT == LARS_F32) {
+              const float4 x0 = *reinterpret_cast<const float4*>(gs), x1 = *reinterpret_cast<const float4*>(gs + 16);
+              x = F8{{x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w}};
+            } else {
+              x = Grad<DT>::widen(*reinterpret_cast<const uint4*>(gs));
+            }
+#pragma unroll
+            for (int t = 0; t < 8; ++t) acc.v[t] += x.v[t];
+          }
+#pragma unroll
+          for (int t = 0; t < 8; ++t) acc.v[t] = wire_saturate<DT>(acc.v[t]);
+          gl.store8(begin + j + i, acc);
+          acc8(ag, acc);
+        }
+      }
+      for (int32_t i = nb + lane; i < n; i += 32) {  // ragged tensor tail (< 8 elements), from global memory
+        const int64_t e = begin + j + i;
+        if (!carried) aw = fma((double)w[e], (double)w[e], aw);
+        const double y = (double)gl.load1(e);
+        ag = fma(y, y, ag);
+      }
+      __syncwarp();  // every lane is done with the stage before lane 0 refills it
+      ++q;
+      produce();
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {  // fixed butterfly: deterministic
+      aw += __shfl_xor_sync(0xffffffffu, aw, o);
+      ag += __shfl_xor_sync(0xffffffffu, ag, o);
+    }
+    if (lane == 0) {
+      const int32_t c = cw0 + kWarps * k;
+      sm_cg[c - c0] = ag;
+      if (!carried) sm_cw[c - c0] = aw;
+    }
+  }
+}
+
+template <class GL, bool REG_PATH = true>  // REG_PATH = false: bulk-copy streaming only (F1 BULK instances)
 __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, const DevScratch& sc, const Hyper& hy,
                                            const float* __restrict__ w, const GL& gl, double* sm_cw,
                                            double* sm_cg, unsigned* sm_done, unsigned* sm_nonfinite, bool carried,
-                                           const StepLr& slr) {
+                                           const StepLr& slr, unsigned char* stages = nullptr,
+                                           uint64_t* bars = nullptr, uint32_t* bulk_q = nullptr) {
   constexpr int kWarps = kThreads / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int32_t s0 = wk.tile_seg[tile], s1 = wk.tile_seg[tile + 1];
@@ -402,10 +592,17 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
   LARS_DCHECK(s0 < s1 || wk.ntensors == 0);
   if (carried && tid < c1 - c0) cp_async8(sm_cw + tid, sc.cpart_wnext + c0 + tid);
   if (lane < 2 && s0 + warp < s1) cp_async16((char*)(sm_si + warp) + 16 * lane, (const char*)(wk.seginfo + s0 + warp) + 16 * lane);
+  bool bulk = false;
+  if constexpr (GL::kBulk) {
+    if (stages) {
+      stream_tile_bulk(c0, c1, wk, w, gl, carried, sm_cw, sm_cg, stages, bars, *bulk_q);
+      bulk = true;
+    }
+  }
   // chunk descriptors are prefetched one iteration ahead (their load would otherwise add a round trip
   // in front of every chunk's data loads)
-  Seg nxt = (c0 + warp < c1) ? wk.chunks[c0 + warp] : Seg{0, 0, 0};
-  for (int32_t c = c0 + warp; c < c1; c += kWarps) {
+  Seg nxt = (REG_PATH && !bulk && c0 + warp < c1) ? wk.chunks[c0 + warp] : Seg{0, 0, 0};
+  for (int32_t c = c0 + warp; REG_PATH && !bulk && c < c1; c += kWarps) {
     const Seg ck = nxt;
     check_chunk(wk, c, ck);
     if (c + kWarps < c1) nxt = wk.chunks[c + kWarps];
@@ -559,14 +756,21 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
 // tile per resident CTA by construction of the work list; dynamically scheduled tiles measured slower).
 // Returns true on thread 0 of the CTA that completed the step's layer count (data-parallel mode: the
 // caller then publishes this rank's C3 shares).
-template <bool CARRY, class GL>
+template <bool CARRY, class GL, bool REG_PATH = true>
 __device__ __forceinline__ bool norms_body(const DevWork& wk, const DevScratch& sc, const Hyper& hy,
-                                           const float* __restrict__ w, const GL& gl) {
+                                           const float* __restrict__ w, const GL& gl,
+                                           unsigned char* stages = nullptr) {
   __shared__ double sm_cw[kMaxTileChunks], sm_cg[kMaxTileChunks];
   __shared__ unsigned sm_done, sm_nonfinite;
+  __shared__ uint64_t sm_bars[kThreads / 32 * kBulkStages];
+  uint32_t bulk_q = 0;  // pieces this warp has consumed (its stages' mbarrier phases)
   if (threadIdx.x == 0) {
     sm_done = 0u;
     sm_nonfinite = 0u;
+  }
+  if (stages && (threadIdx.x & 31) == 0) {
+    for (int i = 0; i < kBulkStages; ++i) mbar_init(sm_bars + (threadIdx.x >> 5) * kBulkStages + i, 1u);
+    mbar_init_fence();
   }
   __syncthreads();
   // carry mode: the previous K2 left sum(w_new^2) per chunk; valid until the host invalidates it
@@ -574,7 +778,8 @@ __device__ __forceinline__ bool norms_body(const DevWork& wk, const DevScratch& 
   const StepLr slr = step_lr(hy);
   for (int32_t tile = blockIdx.x; tile < wk.ntiles; tile += gridDim.x) {
     __syncthreads();  // shared chunk partials of the previous tile fully consumed
-    norms_tile(tile, wk, sc, hy, w, gl, sm_cw, sm_cg, &sm_done, &sm_nonfinite, carried, slr);
+    norms_tile<GL, REG_PATH>(tile, wk, sc, hy, w, gl, sm_cw, sm_cg, &sm_done, &sm_nonfinite, carried, slr, stages,
+                             sm_bars, &bulk_q);
   }
   __syncthreads();
   // Count this CTA's finished layers once; the CTA that completes the count decides the step's skip.
@@ -610,10 +815,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_norms_kernel(DevWor
                                                                           int64_t g_shift) {
   // wait BEFORE releasing the dependent K2: K2 prefetches w and m before its own wait, so it must not
   // become resident while the previous step's K2 may still be writing them
+  extern __shared__ __align__(128) unsigned char k1_stages[];  // kBulkSmem bytes when hy.k1_bulk
   pdl_wait();
   pdl_trigger();
   TRACE_BEGIN
-  norms_body<CARRY>(wk, sc, hy, w, LocalGrad<DT>{g, g_shift});
+  norms_body<CARRY>(wk, sc, hy, w, LocalGrad<DT>{g, g_shift}, hy.k1_bulk ? k1_stages : nullptr);
   TRACE_END(0)
 }
 
@@ -990,10 +1196,12 @@ __device__ int32_t dp_collect_shares(const DevWork& wk, const DevScratch& sc, co
   return out_of_range ? 2 : bad ? 1 : 0;
 }
 
-template <int DT, bool CARRY, int NP>
-__global__ void __launch_bounds__(kThreads, dp_norm_ctas_per_sm(NP)) lars_dp_reduce_norms_kernel(DevWork wk, DevScratch sc,
-                                                                                    Hyper hy, const float* w,
-                                                                                    DpFused f) {
+// BULK: the rank sum streams through bulk-copy stages (stream_tile_bulk; peer reads by the TMA engine, no
+// registers per byte in flight), so every peer-count instance fits 4 CTAs per SM.
+template <int DT, bool CARRY, int NP, bool BULK>
+__global__ void __launch_bounds__(kThreads, BULK ? kCtasPerSm : dp_norm_ctas_per_sm(NP))
+    lars_dp_reduce_norms_kernel(DevWork wk, DevScratch sc, Hyper hy, const float* w, DpFused f) {
+  extern __shared__ __align__(128) unsigned char f1_stages[];  // kBulkSmem bytes when BULK
   TRACE_BEGIN
   pdl_trigger();  // F2's CTAs may be scheduled as F1's retire (they wait in griddepcontrol.wait)
   pdl_wait();
@@ -1031,7 +1239,7 @@ __global__ void __launch_bounds__(kThreads, dp_norm_ctas_per_sm(NP)) lars_dp_red
   gl.begin = f.begin;
   // static tiles (one per CTA): measured faster than 4x finer dynamically scheduled tiles, whose per-tile
   // overhead outweighs the shorter tail (tools/trace_dp.py)
-  const bool final_cta = norms_body<CARRY, PeerSumGrad<DT, NP>>(wk, sc, hy, w, gl);
+  const bool final_cta = norms_body<CARRY, PeerSumGrad<DT, NP>, !BULK>(wk, sc, hy, w, gl, BULK ? f1_stages : nullptr);
   TRACE_MARK(4)
   if (final_cta || (wk.ntensors == 0 && blockIdx.x == 0 && threadIdx.x == 0)) dp_publish_shares(wk, sc, hy, f);
   __syncthreads();
@@ -1104,53 +1312,65 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_dp_update_gather_ke
   }
 }
 
-template <int DT, bool CARRY>
+template <int DT, bool CARRY, bool BULK>
 static void launch_reduce_norms_np(int np, int grid, cudaStream_t st, const DevWork& wk, const DevScratch& sc,
                                    const Hyper& hy, const float* w, const DpFused& f) {
   // cooperative: every CTA waits for CTA 0's entry flag, so the whole grid must be co-resident
+  const size_t smem = BULK ? kBulkSmem : 0;
   if (np <= 2)
-    launch_pdl_ex(lars_dp_reduce_norms_kernel<DT, CARRY, 2>, grid, st, true, wk, sc, hy, w, f);
+    launch_pdl_smem(lars_dp_reduce_norms_kernel<DT, CARRY, 2, BULK>, grid, st, true, smem, wk, sc, hy, w, f);
   else if (np <= 4)
-    launch_pdl_ex(lars_dp_reduce_norms_kernel<DT, CARRY, 4>, grid, st, true, wk, sc, hy, w, f);
+    launch_pdl_smem(lars_dp_reduce_norms_kernel<DT, CARRY, 4, BULK>, grid, st, true, smem, wk, sc, hy, w, f);
   else
-    launch_pdl_ex(lars_dp_reduce_norms_kernel<DT, CARRY, 8>, grid, st, true, wk, sc, hy, w, f);
+    launch_pdl_smem(lars_dp_reduce_norms_kernel<DT, CARRY, 8, BULK>, grid, st, true, smem, wk, sc, hy, w, f);
 }
 
-template <int DT, bool CARRY>
+template <int DT, bool CARRY, bool BULK>
 static int reduce_norms_occupancy_np(int np) {
   int n = 0;
   cudaError_t e;
+  const size_t smem = BULK ? kBulkSmem : 0;
   if (np <= 2)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lars_dp_reduce_norms_kernel<DT, CARRY, 2>, kThreads, 0);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lars_dp_reduce_norms_kernel<DT, CARRY, 2, BULK>, kThreads, smem);
   else if (np <= 4)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lars_dp_reduce_norms_kernel<DT, CARRY, 4>, kThreads, 0);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lars_dp_reduce_norms_kernel<DT, CARRY, 4, BULK>, kThreads, smem);
   else
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lars_dp_reduce_norms_kernel<DT, CARRY, 8>, kThreads, 0);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lars_dp_reduce_norms_kernel<DT, CARRY, 8, BULK>, kThreads, smem);
   return e == cudaSuccess ? n : 0;
 }
 
-int dp_reduce_norms_blocks_per_sm(int32_t dt, bool carry, int np) {
+template <bool BULK>
+static int dp_blocks_per_sm(int32_t dt, bool carry, int np) {
   if (carry) {
-    if (dt == LARS_F32) return reduce_norms_occupancy_np<LARS_F32, true>(np);
-    if (dt == LARS_F16) return reduce_norms_occupancy_np<LARS_F16, true>(np);
-    return reduce_norms_occupancy_np<LARS_BF16, true>(np);
+    if (dt == LARS_F32) return reduce_norms_occupancy_np<LARS_F32, true, BULK>(np);
+    if (dt == LARS_F16) return reduce_norms_occupancy_np<LARS_F16, true, BULK>(np);
+    return reduce_norms_occupancy_np<LARS_BF16, true, BULK>(np);
   }
-  if (dt == LARS_F32) return reduce_norms_occupancy_np<LARS_F32, false>(np);
-  if (dt == LARS_F16) return reduce_norms_occupancy_np<LARS_F16, false>(np);
-  return reduce_norms_occupancy_np<LARS_BF16, false>(np);
+  if (dt == LARS_F32) return reduce_norms_occupancy_np<LARS_F32, false, BULK>(np);
+  if (dt == LARS_F16) return reduce_norms_occupancy_np<LARS_F16, false, BULK>(np);
+  return reduce_norms_occupancy_np<LARS_BF16, false, BULK>(np);
+}
+int dp_reduce_norms_blocks_per_sm(int32_t dt, bool carry, int np, bool bulk) {
+  return bulk ? dp_blocks_per_sm<true>(dt, carry, np) : dp_blocks_per_sm<false>(dt, carry, np);
 }
 
+template <bool BULK>
+static void launch_reduce_norms_b(int32_t dt, bool carry, int np, int grid, cudaStream_t st, const DevWork& wk,
+                                  const DevScratch& sc, const Hyper& hy, const float* w, const DpFused& f) {
+  if (carry) {
+    if (dt == LARS_F32) launch_reduce_norms_np<LARS_F32, true, BULK>(np, grid, st, wk, sc, hy, w, f);
+    else if (dt == LARS_F16) launch_reduce_norms_np<LARS_F16, true, BULK>(np, grid, st, wk, sc, hy, w, f);
+    else launch_reduce_norms_np<LARS_BF16, true, BULK>(np, grid, st, wk, sc, hy, w, f);
+  } else {
+    if (dt == LARS_F32) launch_reduce_norms_np<LARS_F32, false, BULK>(np, grid, st, wk, sc, hy, w, f);
+    else if (dt == LARS_F16) launch_reduce_norms_np<LARS_F16, false, BULK>(np, grid, st, wk, sc, hy, w, f);
+    else launch_reduce_norms_np<LARS_BF16, false, BULK>(np, grid, st, wk, sc, hy, w, f);
+  }
+}
 static void launch_reduce_norms(int32_t dt, bool carry, int np, int grid, cudaStream_t st, const DevWork& wk,
                                 const DevScratch& sc, const Hyper& hy, const float* w, const DpFused& f) {
-  if (carry) {
-    if (dt == LARS_F32) launch_reduce_norms_np<LARS_F32, true>(np, grid, st, wk, sc, hy, w, f);
-    else if (dt == LARS_F16) launch_reduce_norms_np<LARS_F16, true>(np, grid, st, wk, sc, hy, w, f);
-    else launch_reduce_norms_np<LARS_BF16, true>(np, grid, st, wk, sc, hy, w, f);
-  } else {
-    if (dt == LARS_F32) launch_reduce_norms_np<LARS_F32, false>(np, grid, st, wk, sc, hy, w, f);
-    else if (dt == LARS_F16) launch_reduce_norms_np<LARS_F16, false>(np, grid, st, wk, sc, hy, w, f);
-    else launch_reduce_norms_np<LARS_BF16, false>(np, grid, st, wk, sc, hy, w, f);
-  }
+  if (f.bulk) launch_reduce_norms_b<true>(dt, carry, np, grid, st, wk, sc, hy, w, f);
+  else launch_reduce_norms_b<false>(dt, carry, np, grid, st, wk, sc, hy, w, f);
 }
 
 cudaError_t launch_dp_fused(int32_t dt, const DevWork& wk, const DevScratch& sc, const Hyper& hy, float* w, float* m,
@@ -1262,8 +1482,26 @@ cudaError_t launch_init_weights(const DevWork& wk, const InitTable& it, float* w
 template <int DT>
 static cudaError_t launch_norms_t(const DevWork& wk, const DevScratch& sc, const Hyper& hy, const float* w,
                                   const void* g, int64_t g_shift, cudaStream_t st) {
-  if (hy.carry) return launch_pdl(lars_norms_kernel<DT, true>, wk.grid, st, wk, sc, hy, w, g, g_shift);
-  return launch_pdl(lars_norms_kernel<DT, false>, wk.grid, st, wk, sc, hy, w, g, g_shift);
+  const size_t smem = hy.k1_bulk ? kBulkSmem : 0;
+  if (hy.carry) return launch_pdl_smem(lars_norms_kernel<DT, true>, wk.grid, st, false, smem, wk, sc, hy, w, g, g_shift);
+  return launch_pdl_smem(lars_norms_kernel<DT, false>, wk.grid, st, false, smem, wk, sc, hy, w, g, g_shift);
+}
+
+// Resident K1 CTAs per SM with the bulk-copy stages (the work list assumes kCtasPerSm).
+int norms_bulk_blocks_per_sm(int32_t dt, bool carry) {
+  int n = 0;
+  cudaError_t e;
+  const size_t smem = kBulkSmem;
+  if (dt == LARS_F32)
+    e = carry ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lars_norms_kernel<LARS_F32, true>, kThreads, smem)
+              : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lars_norms_kernel<LARS_F32, false>, kThreads, smem);
+  else if (dt == LARS_F16)
+    e = carry ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lars_norms_kernel<LARS_F16, true>, kThreads, smem)
+              : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lars_norms_kernel<LARS_F16, false>, kThreads, smem);
+  else
+    e = carry ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lars_norms_kernel<LARS_BF16, true>, kThreads, smem)
+              : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lars_norms_kernel<LARS_BF16, false>, kThreads, smem);
+  return e == cudaSuccess ? n : 0;
 }
 template <int DT>
 static cudaError_t launch_update_t(const DevWork& wk, const DevScratch& sc, const Hyper& hy, float* w,

@@ -185,7 +185,9 @@ struct lars_ctx {
     int grid_norm = 0, grid_update = 0;
     bool mcast = false;
     int np_template = 0;
+    bool bulk = false;
   } fused;
+  bool k1_bulk = false;     // Hyper::k1_bulk (LARS_K1_BULK)
   int32_t k2_prefetch = 0;  // Hyper::k2_prefetch (LARS_K2_PREFETCH)
   bool k2_prefetch_g = false;
   int32_t last_red_dtype = LARS_F16;
@@ -381,6 +383,13 @@ lars_status_t lars_init(const lars_tensor_t* tensors, int32_t n, const lars_hpar
     if (!g.ok) { delete h; return LARS_ERR_CUDA; }
     int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0) h->sms = sms;
+    // K1 through bulk-copy stages when its shared memory still leaves kCtasPerSm CTAs resident per SM
+    // (the work list has one tile per resident CTA); LARS_K1_BULK=0/1 overrides (A/B measurement)
+    const char* kb = getenv("LARS_K1_BULK");
+    h->k1_bulk = kb ? kb[0] == '1' : kK1BulkDefault;
+    if (h->k1_bulk &&
+        norms_bulk_blocks_per_sm(hp->grad_dtype, (hp->flags & LARS_FLAG_CARRY_WNORM) != 0) < kCtasPerSm)
+      h->k1_bulk = false;
   }
   h->full.wl = make_worklist(h->plan, -1, h->sms * kCtasPerSm, min_tile);
   if (device >= 0) {
@@ -551,6 +560,7 @@ static Hyper hyper(lars_handle_t h, int64_t iter, int64_t* iter_dev = nullptr) {
            (float)h->hp.momentum, (float)h->hp.grad_scale, (h->hp.flags & LARS_FLAG_CARRY_WNORM) != 0,
            (h->hp.flags & LARS_FLAG_LR_AT_APPLY) != 0};
   hy.k2_prefetch = h->k2_prefetch;
+  hy.k1_bulk = h->k1_bulk;
   hy.k2_prefetch_g = h->k2_prefetch_g;
   return hy;
 }
@@ -656,8 +666,14 @@ lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, cons
     // per resident CTA of the instance that will run.
     const char* np_env = getenv("LARS_DP_NP");
     h->fused.np_template = std::min(8, std::max(h->plan.P, np_env ? atoi(np_env) : 0));
-    const int bpsm = dp_reduce_norms_blocks_per_sm(h->hp.grad_dtype, (h->hp.flags & LARS_FLAG_CARRY_WNORM) != 0,
-                                                   h->fused.np_template);
+    const bool carry = (h->hp.flags & LARS_FLAG_CARRY_WNORM) != 0;
+    // F1 through bulk-copy stages (LARS_DP_BULK=0/1 overrides the default) when 4 CTAs per SM stay resident
+    const char* db = getenv("LARS_DP_BULK");
+    h->fused.bulk = db ? db[0] == '1' : kDpBulkDefault;
+    if (h->fused.bulk &&
+        dp_reduce_norms_blocks_per_sm(h->hp.grad_dtype, carry, h->fused.np_template, true) < kCtasPerSm)
+      h->fused.bulk = false;
+    const int bpsm = dp_reduce_norms_blocks_per_sm(h->hp.grad_dtype, carry, h->fused.np_template, h->fused.bulk);
     if (bpsm <= 0) return LARS_ERR_CUDA;
     h->fused.grid_norm = h->sms * bpsm;
     ntiles_target = h->fused.grid_norm;
@@ -900,6 +916,7 @@ static DpFused fused_view(lars_handle_t h, int64_t begin) {
   f.done = (unsigned*)(st + 24);
   f.mcast = h->fused.mcast;
   f.np_template = h->fused.np_template;
+  f.bulk = h->fused.bulk;
   f.hwin = h->hwin;
   return f;
 }
