@@ -253,13 +253,17 @@ def run_ours(args):
             nvl = None
     barrier()
     torch.cuda.synchronize()
-    nvl0 = nvl.read() if nvl else None
+    if nvl:
+        nvl.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     run(args.steps)
     e1.record(stream)
     torch.cuda.synchronize()
-    nvl1 = nvl.read() if nvl else None
+    try:
+        nvl1 = nvl.stop() if nvl else None
+    except Exception:  # noqa: BLE001 - counters are evidence, not part of the step
+        nvl1 = None
     barrier()
     clk = clocks.stop()
     ms_total = max_over_ranks(e0.elapsed_time(e1))
@@ -395,10 +399,11 @@ def run_ours(args):
                 "step_frac_of_bus_roofline": round(bus / NVLINK_PEER_GBS / 1e9 / (ms_step * 1e-3), 4),
                 # north_star framing: 900 GB/s per direction nominal NVLink 5 beside the measured peer copy
                 "frac_of_nominal": round(ach / NVLINK_NOMINAL_GBS, 4), "nominal_peak": NVLINK_NOMINAL_GBS}
-    if nvl0 and nvl1:  # this rank's link payload per step vs the algorithmic bus bytes (RS in + AG out)
+    if nvl1:  # this rank's link traffic per step (hardware counters) vs the algorithmic bus bytes
         roof["nvlink_counters"] = {
-            "tx_bytes_per_step": int((nvl1["tx"] - nvl0["tx"]) / args.steps),
-            "rx_bytes_per_step": int((nvl1["rx"] - nvl0["rx"]) / args.steps),
+            "tx_bytes_per_step": int(nvl1["tx"] / args.steps),
+            "rx_bytes_per_step": int(nvl1["rx"] / args.steps),
+            "interval_s": round(nvl1["seconds"], 6), "timed_region_s": round(ms_total * 1e-3, 6),
             # each direction of a GPU's links carries (P-1)/P * (gbytes + 4) * N per step: the shard pulls
             # (RS) and the weight stores (AG) leave on one direction and arrive on the other
             "algorithmic_bytes_per_direction": int(bus),
@@ -435,7 +440,7 @@ def run_ours(args):
     if P == 1 and rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(lay, w_host, [g_host], m_host, dtype, P)
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        emit(out)
     if P > 1:
         dist.destroy_process_group()
     del np
@@ -506,11 +511,27 @@ def run_reference(args):
            "cpu_baseline": {"value": round(value, 1), "unit": "params/s", "cores": 1, "kind": "oracle",
                             "cpu": cpu_model(), "sample": sample},
            "e2e": {"value": round(value, 1), "unit": "params/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    emit(out)
+
+
+_JSON_OUT = None
+
+
+def emit(out: dict) -> None:
+    """The one JSON line, on the process's real stdout (everything else written to fd 1 goes to stderr)."""
+    f = _JSON_OUT or sys.stdout
+    f.write(json.dumps(out) + "\n")
+    f.flush()
 
 
 def main():
-    # NCCL's own banner ("NCCL version ...") goes to stderr: stdout carries exactly one JSON line
+    global _JSON_OUT
+    # stdout carries exactly one JSON line: fd 1 is pointed at stderr for the whole run, so banners printed by
+    # native libraries (NCCL's "NCCL version ...") cannot land on it; the JSON goes to a duplicate of the
+    # original stdout
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     args = parse()
     if args.impl == "reference":

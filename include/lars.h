@@ -229,9 +229,11 @@ lars_status_t lars_step(lars_handle_t h, float* w, const void* g, float* m, int6
 lars_status_t lars_step_dev_iter(lars_handle_t h, float* w, const void* g, float* m, int64_t* iter_dev, void* stream);
 
 /* Same as lars_step, but the gradient comes from HOST memory g_host (pinned for async copies,
- * padded_numel elements of grad_dtype): the library copies it into its own device staging buffer on
- * `stream`, runs the step, and copies the step status + per-layer norms back into library-owned
- * pinned memory (read them with lars_last_step_skipped / lars_last_norms). */
+ * padded_numel elements of grad_dtype): the library copies it into one of two device staging buffers on its
+ * own copy stream (ordered before the step on `stream` by an event; the copy for the next call overlaps this
+ * step's kernels), runs the step on `stream`, and copies the step status + per-layer norms back into
+ * library-owned pinned memory (read them with lars_last_step_skipped / lars_last_norms). g_host must stay
+ * unmodified until the step has completed on `stream`. */
 lars_status_t lars_step_host_grad(lars_handle_t h, float* w, const void* g_host, float* m,
                                   int64_t iter, void* stream);
 

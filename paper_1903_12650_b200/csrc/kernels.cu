@@ -1129,16 +1129,27 @@ __global__ void lars_split_finish_kernel(DevWork wk, DevScratch sc, Hyper hy) { 
 // Gradient and weight buffers live in NCCL symmetric windows (ncclMemAlloc + ncclCommWindowRegister), so
 // every rank can load and store every other rank's buffers over NVLink with plain ld/st (LSA pointers).
 // The reduce-scatter is fused into K1 (each rank sums its shard over all ranks' gradients in fp32), the
-// C3 exchange rides on F1's tail and F2's head (flagged slots, no extra kernel), and the all-gather is fused into K2 (each
-// updated weight is stored locally and into every peer). Per-CTA LSA barriers order the phases.
+// C3 exchange rides on F1's tail and F2's head (epoch-tagged words, no extra kernel), and the all-gather is fused
+// into K2 (each updated weight is stored locally and into every peer). One LSA barrier at F1's entry (taken by
+// CTA 0) and one at F2's exit (taken by the last CTA) order the steps across ranks.
 //
 //   F1 lars_dp_reduce_norms_kernel : barrier(b) -> shard sum over ranks + norms; the final CTA publishes
-//                                    this rank's C3 shares into every rank's exchange slot (epoch-flagged)
+//                                    this rank's C3 shares into every rank's exchange slot (epoch-tagged words)
 //   F2 lars_dp_update_gather_kernel: wait for all ranks' shares, fixed-order sum, finish split layers, skip
 //                                    -> update + store w to every peer -> barrier(b)
-// End of F1 (one thread): this rank's C3 shares [non-finite flag, split-layer sums] go into slot [rank] of
-// every rank's exchange window, then the slot's epoch word is released. The iteration of this step is
-// recorded (and a device iteration advanced) here, after every layer of this rank has read it.
+// The C3 shares [non-finite flag, split-layer sums] travel as EPOCH-TAGGED words: value i of rank p lands in
+// slot p of every rank's exchange window as two 64-bit words, (epoch << 32) | low 32 bits and
+// (epoch << 32) | high 32 bits of the double. Every word is written and read whole (single-copy atomic), so
+// a reader that sees the step's epoch in a word has that word's payload: no release fence and no separate
+// flag, i.e. no NVLink round trip on the critical path between F1's last tile and F2's start (the
+// fence + flag protocol cost ~4 us here). Epochs only grow (the 32-bit tag wraps after 4e9 steps).
+__device__ __forceinline__ unsigned long long share_word(uint32_t epoch, uint32_t half) {
+  return ((unsigned long long)epoch << 32) | half;
+}
+
+// End of F1 (one thread): this rank's shares go into slot [rank] of every rank's exchange window. The
+// iteration of this step is recorded (and a device iteration advanced) here, after every layer of this rank
+// has read it.
 __device__ void dp_publish_shares(const DevWork& wk, const DevScratch& sc, const Hyper& hy, const DpFused& f) {
   const int32_t n = 1 + 2 * wk.nsplit_total;
   const unsigned long long epoch = *f.epoch + 1ull;
@@ -1146,37 +1157,43 @@ __device__ void dp_publish_shares(const DevWork& wk, const DevScratch& sc, const
   const int64_t t = hy.iter_dev ? *(volatile int64_t*)hy.iter_dev : hy.iter;
   *f.step_iter = t;
   if (hy.iter_dev) *(volatile int64_t*)hy.iter_dev = t + 1;
-  for (int p = 0; p < f.nranks; ++p) {  // payloads to every rank first, then one fence, then the flags
-    double* slot = (double*)ncclGetLsaPointer(f.xwin, (size_t)f.rank * (n + 1) * sizeof(double), p);
-    for (int32_t i = 0; i < n; ++i) slot[1 + i] = sc.c3[i];
-  }
-  cuda::atomic_thread_fence(cuda::memory_order_release, cuda::thread_scope_system);
+  const uint32_t e32 = (uint32_t)epoch;
   for (int p = 0; p < f.nranks; ++p) {
-    double* slot = (double*)ncclGetLsaPointer(f.xwin, (size_t)f.rank * (n + 1) * sizeof(double), p);
-    cuda::atomic_ref<unsigned long long, cuda::thread_scope_system> flag(*(unsigned long long*)slot);
-    flag.store(epoch, cuda::memory_order_relaxed);
+    unsigned long long* slot =
+        (unsigned long long*)ncclGetLsaPointer(f.xwin, (size_t)f.rank * 2 * n * sizeof(unsigned long long), p);
+    for (int32_t i = 0; i < n; ++i) {
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(sc.c3[i]);
+      cuda::atomic_ref<unsigned long long, cuda::thread_scope_system> lo(slot[2 * i]), hi(slot[2 * i + 1]);
+      lo.store(share_word(e32, (uint32_t)bits), cuda::memory_order_relaxed);
+      hi.store(share_word(e32, (uint32_t)(bits >> 32)), cuda::memory_order_relaxed);
+    }
   }
   for (int32_t i = 0; i < n; ++i) sc.c3[i] = 0.0;  // next step's shares start from zero
 }
 
-// Start of F2 (warp 0 of every CTA): wait for every rank's shares of this step, sum them in rank order
-// (identical on every rank), finish the split layers this rank touches, decide the skip. Returns the
-// step status (0 apply, 1 non-finite, 2 iteration out of range) to every lane of warp 0.
+// Start of F2 (warp 0 of every CTA): wait until every word of every rank's shares carries this step's
+// epoch, sum the shares in rank order (identical on every rank), finish the split layers this rank touches,
+// decide the skip. Returns the step status (0 apply, 1 non-finite, 2 iteration out of range) to every lane
+// of warp 0.
 __device__ int32_t dp_collect_shares(const DevWork& wk, const DevScratch& sc, const Hyper& hy, const DpFused& f) {
   const int lane = threadIdx.x & 31;
   const int32_t n = 1 + 2 * wk.nsplit_total;
-  const unsigned long long epoch = *(volatile unsigned long long*)f.epoch;
-  const double* x = (const double*)ncclGetLocalPointer(f.xwin, 0);
-  if (lane < f.nranks) {
-    cuda::atomic_ref<const unsigned long long, cuda::thread_scope_system> flag(
-        *(const unsigned long long*)(x + (size_t)lane * (n + 1)));
-    while (flag.load(cuda::memory_order_acquire) < epoch) __nanosleep(64);
+  const uint32_t e32 = (uint32_t)*(volatile unsigned long long*)f.epoch;
+  unsigned long long* x = (unsigned long long*)ncclGetLocalPointer(f.xwin, 0);
+  for (int32_t k = lane; k < f.nranks * 2 * n; k += 32) {
+    cuda::atomic_ref<unsigned long long, cuda::thread_scope_system> word(x[k]);
+    while ((uint32_t)(word.load(cuda::memory_order_relaxed) >> 32) != e32) __nanosleep(32);
   }
   __syncwarp();
+  auto val = [&](int p, int32_t i) {  // every word of this step is in: plain reads
+    const unsigned long long* w = x + ((size_t)p * n + i) * 2;
+    const unsigned long long lo = *(volatile const unsigned long long*)w, hi = *(volatile const unsigned long long*)(w + 1);
+    return __longlong_as_double((long long)((hi << 32) | (lo & 0xffffffffull)));
+  };
   bool bad = false;
   for (int32_t i = lane; i < n; i += 32) {
     double tot = 0.0;
-    for (int p = 0; p < f.nranks; ++p) tot += x[(size_t)p * (n + 1) + 1 + i];  // rank order
+    for (int p = 0; p < f.nranks; ++p) tot += val(p, i);  // rank order
     bad |= (i == 0) ? (tot > 0.0) : !isfinite(tot);
   }
   Hyper h2 = hy;  // the step's iteration as recorded by F1 (a device iteration has moved on already)
@@ -1186,8 +1203,8 @@ __device__ int32_t dp_collect_shares(const DevWork& wk, const DevScratch& sc, co
     const int32_t l = wk.split_locals[k], j = wk.tsplit[l];
     double sw = 0.0, sg = 0.0;
     for (int p = 0; p < f.nranks; ++p) {
-      sw += x[(size_t)p * (n + 1) + 2 + 2 * j];
-      sg += x[(size_t)p * (n + 1) + 3 + 2 * j];
+      sw += val(p, 1 + 2 * j);
+      sg += val(p, 2 + 2 * j);
     }
     bad |= finish_core(l, sw, sg, wk, sc, h2);  // identical values from every CTA (benign duplicate stores)
   }

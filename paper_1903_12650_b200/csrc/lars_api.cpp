@@ -169,6 +169,12 @@ struct lars_ctx {
   void* gred = nullptr;
   void* gstage = nullptr;
   void* pinned = nullptr;  // host mirror of skip + norms for lars_step_host_grad
+  // lars_step_host_grad: two staging buffers filled on a copy stream, so the copy of step t+1's gradient
+  // overlaps step t's kernels (consumed[b]: the step that read buffer b is done; copied[b]: its copy is)
+  void* hstage[2] = {nullptr, nullptr};
+  cudaStream_t hcs = nullptr;
+  cudaEvent_t hcopied[2] = {nullptr, nullptr}, hconsumed[2] = {nullptr, nullptr};
+  int hnext = 0;
   cudaStream_t last_stream = nullptr;
   const DevBufs* last = nullptr;
   Profiler prof;
@@ -280,8 +286,8 @@ static bool fused_eligible(lars_ctx* h) {
 static lars_status_t setup_fused(lars_ctx* h) {
   auto& f = h->fused;
   const size_t wb = round4k((size_t)h->plan.padded * 4), gb = round4k((size_t)h->plan.padded * dtype_size(h->hp.grad_dtype));
-  // exchange slot per rank: [epoch | non-finite flag | split-layer sums]
-  const size_t xb = round4k((size_t)h->plan.P * (2 + 2 * (size_t)h->plan.nsplit) * sizeof(double));
+  // exchange slot per rank: [non-finite flag, split-layer sums], each value as two epoch-tagged 64-bit words
+  const size_t xb = round4k((size_t)h->plan.P * 2 * (1 + 2 * (size_t)h->plan.nsplit) * sizeof(uint64_t));
   NCCL_OR(ncclMemAlloc(&f.w, wb));
   NCCL_OR(ncclMemAlloc(&f.g, gb));
   NCCL_OR(ncclMemAlloc(&f.x, xb));
@@ -614,10 +620,32 @@ lars_status_t lars_step_host_grad(lars_handle_t h, float* w, const void* g_host,
   if (h->device < 0) return LARS_ERR_NO_DEVICE;
   DeviceGuard dg(h->device);
   cudaStream_t s = (cudaStream_t)stream;
-  lars_status_t st = stage_host_grad(h, g_host, s);
+  lars_status_t st = check_step_args(h, w, w, m, iter);  // (g is staged: validated below)
   if (st != LARS_OK) return st;
-  st = lars_step(h, w, h->gstage, m, iter, stream);
+  const size_t gbytes = (size_t)h->plan.padded * dtype_size(h->hp.grad_dtype);
+  if (!h->hcs) {
+    for (int b = 0; b < 2; ++b) {
+      if (cudaMalloc(&h->hstage[b], gbytes) != cudaSuccess) { h->hstage[b] = nullptr; return LARS_ERR_OOM; }
+      CUDA_OR(cudaEventCreateWithFlags(&h->hcopied[b], cudaEventDisableTiming));
+      CUDA_OR(cudaEventCreateWithFlags(&h->hconsumed[b], cudaEventDisableTiming));
+      CUDA_OR(cudaEventRecord(h->hconsumed[b], s));
+    }
+    if (!h->pinned && cudaMallocHost(&h->pinned, 256 + 2 * (size_t)h->plan.L * sizeof(double)) != cudaSuccess) {
+      h->pinned = nullptr;
+      return LARS_ERR_OOM;
+    }
+    CUDA_OR(cudaStreamCreateWithFlags(&h->hcs, cudaStreamNonBlocking));
+  }
+  const int b = h->hnext;
+  h->hnext ^= 1;
+  // the copy waits only for the step that last read this buffer (two steps ago), not for step t-1
+  CUDA_OR(cudaStreamWaitEvent(h->hcs, h->hconsumed[b], 0));
+  CUDA_OR(cudaMemcpyAsync(h->hstage[b], g_host, gbytes, cudaMemcpyHostToDevice, h->hcs));
+  CUDA_OR(cudaEventRecord(h->hcopied[b], h->hcs));
+  CUDA_OR(cudaStreamWaitEvent(s, h->hcopied[b], 0));
+  st = lars_step(h, w, h->hstage[b], m, iter, stream);
   if (st != LARS_OK) return st;
+  CUDA_OR(cudaEventRecord(h->hconsumed[b], s));
   return readback_status(h, h->full, s);
 }
 
@@ -1182,6 +1210,15 @@ lars_status_t lars_destroy(lars_handle_t h) {
     cudaFree(h->shard.mem);
     cudaFree(h->gred);
     cudaFree(h->gstage);
+    if (h->hcs) {
+      cudaStreamSynchronize(h->hcs);
+      cudaStreamDestroy(h->hcs);
+    }
+    for (int b = 0; b < 2; ++b) {
+      cudaFree(h->hstage[b]);
+      if (h->hcopied[b]) cudaEventDestroy(h->hcopied[b]);
+      if (h->hconsumed[b]) cudaEventDestroy(h->hconsumed[b]);
+    }
     cudaFree(h->init_mem);
     if (h->pinned) cudaFreeHost(h->pinned);
     for (auto& st : h->prof.pending)

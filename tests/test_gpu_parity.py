@@ -195,6 +195,22 @@ def test_host_gradient_entry_point():
     torch.cuda.synchronize()
     assert torch.equal(a.w, b.w) and torch.equal(a.m, b.m)
     assert not b.h.last_step_skipped()
+    # consecutive host-gradient steps, issued without synchronizing: the library's two staging buffers and
+    # copy stream (the next step's copy overlaps this step) give bitwise the device-gradient result, and a
+    # non-finite host gradient still skips its own step only
+    hosts = [torch.from_numpy(G.pack(G.grads(lay, 0, 3 + k, "f16"), b.h.offsets, b.h.padded_numel)).pin_memory()
+             for k in range(5)]
+    hosts[3][b.h.offsets[2] + 1] = float("nan")
+    for k in range(5):
+        b.h.lars_step_host_grad(b.w, hosts[k], b.m, 82 + k)
+    torch.cuda.synchronize()
+    assert not b.h.last_step_skipped()
+    for k in range(5):
+        a.g.copy_(hosts[k])
+        a.step(82 + k)
+        torch.cuda.synchronize()
+        assert a.h.last_step_skipped() == (k == 3)
+    assert torch.equal(a.w, b.w) and torch.equal(a.m, b.m)
 
 
 def test_device_argument_errors():

@@ -21,6 +21,11 @@ for v in 0 1; do
     --master-addr=127.0.0.1 --master-port=$((29900 + v)) bench.py --gpus $N > "$out/bench_bulk$v.json" 2> "$out/bench_bulk$v.err"
   echo "bench --gpus $N LARS_DP_BULK=$v rc=$?" >> "$out/status"
 done
+# the 8-peer F1 instance through bench.py's whole argument/launch/JSON path (absent peers predicated off)
+LARS_DP_NP=8 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N \
+  --master-addr=127.0.0.1 --master-port=29910 bench.py --gpus $N --steps 100 --warmup 10 --e2e-steps 5 \
+  > "$out/bench_np8.json" 2> "$out/bench_np8.err"
+echo "bench --gpus $N LARS_DP_NP=8 rc=$?" >> "$out/status"
 if [ -f build/liblars_trace.so ]; then
   for v in 0 1; do
     LARS_DP_BULK=$v timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N \
@@ -28,3 +33,10 @@ if [ -f build/liblars_trace.so ]; then
     echo "trace_dp LARS_DP_BULK=$v rc=$?" >> "$out/status"
   done
 fi
+python - > "$out/nvlink_probe.txt" 2>&1 <<'PY'
+import sys, time; sys.path.insert(0, ".")
+from tools.nvlink_counters import NvlinkCounters
+n = NvlinkCounters(0)
+print(n.describe())
+n.start(); time.sleep(0.2); print(n.stop())
+PY
