@@ -103,7 +103,8 @@ typedef struct {
   double eps;            /* trust-ratio denominator guard >= 0 (default 0)                        */
   double warmup_epochs;  /* W = round-half-up(warmup_epochs * ipe) iterations (default 5)         */
   double poly_power;     /* p >= 0 (p = 1 linear, p = 0 constant; default 2)                       */
-  double grad_scale;     /* s: G = s * sum_r g_r (default 1.0; e.g. 1/(P*loss_scale))             */
+  double grad_scale;     /* s: G = s * sum_r g_r (default 1.0; e.g. 1/(P*loss_scale)); finite,
+                          * nonzero, |s| <= 2^64, else lars_init returns LARS_ERR_INVALID_ARG    */
   int64_t global_batch;  /* B > 0 (default 81,920)                                    */
   int64_t dataset_size;  /* D > 0 images per epoch (default 1,280,000)               */
   int32_t total_epochs;  /* E > 0 (default 90)                                   */

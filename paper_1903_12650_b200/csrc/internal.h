@@ -43,6 +43,7 @@ constexpr int kNormUnroll = LARS_NORM_UNROLL;  // K1 vector groups per lane per 
 constexpr int32_t kDefaultMinTile = 4096;
 constexpr bool kK1BulkDefault = false;  // K1 bulk-copy streaming (Hyper::k1_bulk) unless LARS_K1_BULK says
 constexpr bool kDpBulkDefault = false;  // F1 bulk-copy streaming (DpFused::bulk) unless LARS_DP_BULK says
+constexpr bool kDeferDefault = true;  // lars_step: layer finish in K2's prologue unless LARS_DEFER_FINISH=0
 constexpr int32_t kChunk = 2048;        // elements per warp work item (multiple of 256)
 
 // One contiguous piece of one tensor inside one work tile. begin is a flat element offset,
@@ -162,6 +163,10 @@ struct DevScratch {
   double* lambda;        // trust ratio
   float* coef;           // lr(t) * lambda, as K2 uses it
   float* beta;           // per-tensor weight decay (0 for skip kinds)
+  // Deferred finish (single GPU, Hyper::defer): K1 leaves only segment partials, a non-finite flag per K1
+  // CTA and (device iteration) the step's iteration; K2 finishes the layers of its own tile.
+  int32_t* nf_cta;       // per K1 CTA: 1 if one of its segment partials is non-finite
+  int64_t* step_iter;    // the iteration K1 saw in *iter_dev
 };
 
 struct Hyper {
@@ -177,6 +182,7 @@ struct Hyper {
   int32_t k2_prefetch = 0;   // K2: chunks per CTA whose w, m are prefetched into L2 before its PDL wait
   bool k2_prefetch_g = false;  // ... and their gradient
   bool k1_bulk = false;      // K1 streams its chunks through the bulk-copy engine (stream_tile_bulk)
+  bool defer = false;        // single GPU: the layer finish moves from K1's tail into K2's prologue
 };
 
 // g_shift: the gradient of flat element e is g[e - g_shift] (the DP step reads its reduced shard).

@@ -704,6 +704,14 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
     const int32_t l = si.tensor;
     const int32_t nseg = si.nseg;
     const int32_t split = si.split;
+    if (hy.defer) {  // K2 finishes the layer: leave the segment partial (and whether it is finite)
+      if (lane == 0) {
+        sc.part_w[s] = tw;
+        sc.part_g[s] = tg;
+        if (!(isfinite(tw) && isfinite(tg))) atomicOr(sm_nonfinite, 1u);
+      }
+      continue;
+    }
     if (nseg == 1) {
       if (lane == 0) {
         if (split >= 0) {  // straddles ranks: publish this rank's share for the C3 allreduce
@@ -782,6 +790,13 @@ __device__ __forceinline__ bool norms_body(const DevWork& wk, const DevScratch& 
                              sm_bars, &bulk_q);
   }
   __syncthreads();
+  if (hy.defer) {  // no cross-CTA finish here: one flag per CTA, and the iteration K2 will use
+    if (threadIdx.x == 0) {
+      sc.nf_cta[blockIdx.x] = sm_nonfinite ? 1 : 0;
+      if (blockIdx.x == 0 && hy.iter_dev) *sc.step_iter = *(volatile const int64_t*)hy.iter_dev;
+    }
+    return false;
+  }
   // Count this CTA's finished layers once; the CTA that completes the count decides the step's skip.
   if (threadIdx.x == 0 && sm_done > 0u) {
     if (sm_nonfinite) atomicOr(sc.nonfinite, 1u);
@@ -954,15 +969,23 @@ struct McastWeights {
 // One warp chunk of K2 (and F2): unscale + weight decay + momentum + update of <= kChunk elements, every new
 // weight also handed to `ws` (the other ranks' buffers on the fused path); carry mode also leaves the chunk's
 // sum(w_new^2) for the next step's K1.
+// Per-layer coefficients K2 reads: lr*lambda and beta_l of local tensor l at coef[l - base], beta[l - base]
+// (the scratch arrays, base 0; or, deferred finish, the CTA's shared copies for its tile's layers).
+struct Coefs {
+  const float* coef;
+  const float* beta;
+  int32_t base;
+};
+
 template <int DT, bool CARRY, typename WS = NoPeers>
 __device__ __forceinline__ void update_chunk(int32_t c, const DevWork& wk, const DevScratch& sc, const Hyper& hy,
                                              float* __restrict__ w, const void* __restrict__ g, int64_t g_shift,
-                                             float* __restrict__ m, const WS& ws = WS()) {
+                                             float* __restrict__ m, const WS& ws, const Coefs& cs) {
   const int lane = threadIdx.x & 31;
   const float s = hy.grad_scale_f, mu = hy.mu;
   const Seg ck = wk.chunks[c];
   check_chunk(wk, c, ck);
-  const float cf = sc.coef[ck.tensor], b = sc.beta[ck.tensor];
+  const float cf = cs.coef[ck.tensor - cs.base], b = cs.beta[ck.tensor - cs.base];
   float* wp = w + ck.begin;
   float* mp = m + ck.begin;
   const int64_t gi = ck.begin - g_shift;
@@ -1017,7 +1040,8 @@ __device__ __forceinline__ void update_chunk(int32_t c, const DevWork& wk, const
 template <int DT, bool CARRY, typename WS = NoPeers>
 __device__ __forceinline__ void update_item(int32_t item, const DevWork& wk, const DevScratch& sc, const Hyper& hy,
                                             float* __restrict__ w, const void* __restrict__ g, int64_t g_shift,
-                                            float* __restrict__ m, const WS& ws = WS()) {
+                                            float* __restrict__ m, const WS& ws = WS(), Coefs cs = Coefs{}) {
+  if (!cs.coef) cs = Coefs{sc.coef, sc.beta, 0};
   constexpr int kWarps = kThreads / 32;
   const int warp = threadIdx.x >> 5;
   // item -> (part q, tile): all tiles' last parts first (the bytes K1 read last, still in L2), then the
@@ -1028,7 +1052,7 @@ __device__ __forceinline__ void update_item(int32_t item, const DevWork& wk, con
   const int32_t c1 = t0 + (int32_t)((int64_t)tn * (q + 1) / kUpdateSplit);
   LARS_DCHECK(tile >= 0 && tile < wk.ntiles && q >= 0 && q < kUpdateSplit && c0 <= c1 && c1 <= wk.nchunks);
   for (int32_t c = c1 - 1 - warp; c >= c0; c -= kWarps)  // backwards: K1's most recent reads first
-    update_chunk<DT, CARRY, WS>(c, wk, sc, hy, w, g, g_shift, m, ws);
+    update_chunk<DT, CARRY, WS>(c, wk, sc, hy, w, g, g_shift, m, ws, cs);
 }
 
 // Before K2's griddepcontrol.wait (its CTAs become resident as K1's retire): the bulk-copy engine
@@ -1055,6 +1079,68 @@ __device__ __forceinline__ void k2_prefetch_first(const DevWork& wk, const Hyper
   }
 }
 
+// Deferred finish (single GPU, hy.defer), start of K2 after griddepcontrol.wait: K1 has left every
+// segment's partial sums, one non-finite flag per K1 CTA and (device iteration) the step's iteration.
+// The step is skipped when any flag is set (a layer norm is non-finite exactly when one of its partials is:
+// the partials are sums of <= 2^31 fp32 squares and |s| <= 2^64, so no finite sum overflows the norm) or the
+// iteration is out of range; every CTA takes the same decision, CTA 0 records it and advances a device
+// iteration (every K1 CTA has read it; the next K1 reads it after this grid completes).
+__device__ __forceinline__ bool deferred_skip(const DevWork& wk, const DevScratch& sc, const Hyper& hy) {
+  int bad = 0;
+  for (int32_t i = threadIdx.x; i < wk.grid; i += blockDim.x) bad |= __ldcg(sc.nf_cta + i);
+  bad = __syncthreads_or(bad);
+  const int64_t t = hy.iter_dev ? __ldcg(sc.step_iter) : hy.iter;
+  const bool in_range = t >= 0 && t < hy.total_iters;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *(volatile int32_t*)sc.skip = !in_range ? 2 : bad ? 1 : 0;
+    if (hy.iter_dev) *(volatile int64_t*)hy.iter_dev = t + 1;
+  }
+  return bad || !in_range;
+}
+
+// The layers of `tile` (its segments s0..s1-1, one per layer, consecutive local tensor ids): each layer's
+// norms from ALL its segment partials in the same fixed order as K1's own finish (lane-strided sum, xor
+// butterfly: every CTA that touches the layer computes the same bits), then lambda and lr*lambda into the
+// CTA's shared arrays (index = tensor - base, base returned). The CTA holding a layer's first segment also
+// writes the layer's outputs (lars_last_norms).
+__device__ __forceinline__ int32_t deferred_finish_tile(int32_t tile, const DevWork& wk, const DevScratch& sc,
+                                                        const Hyper& hy, float* sm_coef, float* sm_beta) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int32_t s0 = wk.tile_seg[tile], s1 = wk.tile_seg[tile + 1];
+  const int32_t base = wk.seginfo[s0].tensor;
+  const int64_t t = hy.iter_dev ? __ldcg(sc.step_iter) : hy.iter;
+  const bool in_range = t >= 0 && t < hy.total_iters;
+  const double lr = in_range ? hy.lr_table[t] : 0.0;
+  for (int32_t s = s0 + warp; s < s1; s += kThreads / 32) {
+    const SegInfo si = wk.seginfo[s];
+    LARS_DCHECK(si.tensor - base == s - s0 && si.tensor - base < kMaxTileChunks);
+    double sw, sg;
+    warp_sum2(sc.part_w, sc.part_g, si.tseg_begin, si.tseg_begin + si.nseg, lane, sw, sg);
+    if (lane == 0) {
+      const double wn = sqrt(sw), gn = fabs(hy.grad_scale) * sqrt(sg);
+      double lam = 1.0, beta = 0.0;
+      if (si.lars) {  // reading #1, #3, #4 (same arithmetic as finish_core)
+        beta = hy.weight_decay;
+        const double den = gn + hy.weight_decay * wn + hy.eps;
+        if (wn > 0.0 && den > hy.eps) lam = hy.eta * wn / den;
+      }
+      const float cf = in_range ? (float)(lr * lam) : 0.0f;
+      sm_coef[s - s0] = cf;
+      sm_beta[s - s0] = (float)beta;
+      if (s == si.tseg_begin) {
+        const int32_t l = si.tensor;
+        sc.w_norm[l] = wn;
+        sc.g_norm[l] = gn;
+        sc.lambda[l] = lam;
+        sc.coef[l] = cf;
+        sc.beta[l] = (float)beta;
+      }
+    }
+  }
+  __syncthreads();
+  return base;
+}
+
 // K2. Same persistent schedule as K1 (CTA b owns tiles b, b + grid, ...; identical grid and resources,
 // so CTA b runs on the same SM in both kernels) and each tile's chunks walked backwards: the gradient
 // bytes K1 streamed last into this SM's L2 slice are re-read first.
@@ -1067,16 +1153,30 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_update_kernel(DevWo
   // K1 writes none of w, g, m: while K1 drains, pull the first chunks this CTA updates into L2
   if (hy.k2_prefetch > 0) k2_prefetch_first<DT>(wk, hy, w, g, g_shift, m);
   pdl_wait();
-  const bool skip = *(volatile const int32_t*)sc.skip != 0;  // whole step skipped (non-finite norm)
+  bool skip;
   TRACE_BEGIN
-  if (!skip)
-    for (int32_t tile = blockIdx.x; tile < wk.ntiles; tile += gridDim.x)
-      for (int32_t q = kUpdateSplit - 1; q >= 0; --q)
-        if constexpr (HALF)
-          update_item<DT, CARRY, LocalHalf<DT>>((kUpdateSplit - 1 - q) * wk.ntiles + tile, wk, sc, hy, w, g,
-                                                g_shift, m, LocalHalf<DT>{(uint16_t*)hy.w_half});
-        else
-          update_item<DT, CARRY>((kUpdateSplit - 1 - q) * wk.ntiles + tile, wk, sc, hy, w, g, g_shift, m);
+  if (!HALF && hy.defer) {
+    skip = deferred_skip(wk, sc, hy);
+    for (int32_t tile = blockIdx.x; tile < wk.ntiles; tile += gridDim.x) {
+      __shared__ float sm_coef[kMaxTileChunks], sm_beta[kMaxTileChunks];
+      const int32_t base = deferred_finish_tile(tile, wk, sc, hy, sm_coef, sm_beta);
+      if (!skip)
+        for (int32_t q = kUpdateSplit - 1; q >= 0; --q)
+          update_item<DT, CARRY>((kUpdateSplit - 1 - q) * wk.ntiles + tile, wk, sc, hy, w, g, g_shift, m, NoPeers(),
+                                 Coefs{sm_coef, sm_beta, base});
+      __syncthreads();  // the tile's coefficients are consumed before the next tile's overwrite them
+    }
+  } else {
+    skip = *(volatile const int32_t*)sc.skip != 0;  // whole step skipped (non-finite norm)
+    if (!skip)
+      for (int32_t tile = blockIdx.x; tile < wk.ntiles; tile += gridDim.x)
+        for (int32_t q = kUpdateSplit - 1; q >= 0; --q)
+          if constexpr (HALF)
+            update_item<DT, CARRY, LocalHalf<DT>>((kUpdateSplit - 1 - q) * wk.ntiles + tile, wk, sc, hy, w, g,
+                                                  g_shift, m, LocalHalf<DT>{(uint16_t*)hy.w_half});
+          else
+            update_item<DT, CARRY>((kUpdateSplit - 1 - q) * wk.ntiles + tile, wk, sc, hy, w, g, g_shift, m);
+  }
   if constexpr (HALF)
     if (skip) publish_half_tiles(wk, w, LocalHalf<DT>{(uint16_t*)hy.w_half});
   // every chunk's sum(w_new^2) is written once this grid completes; the next K1 (stream-ordered after

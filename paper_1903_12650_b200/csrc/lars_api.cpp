@@ -70,6 +70,8 @@ lars_status_t upload(DevBufs& b, int sms, int32_t nsplit_total, bool dp, int64_t
   add(nt, 4); add(nt, 4); add(dp ? 1 + 2 * (size_t)nsplit_total : 1, 8);                // split layers, C3
   add(ns, 8); add(ns, 8); add(nt, 4); add(1, 4); add(1, 4); add(1, 4);                  // partials, counters
   add(nt, 8); add(nt, 8); add(nt, 8); add(nt, 4); add(nt, 4);                           // outputs
+  const size_t ngrid = std::max<size_t>((size_t)std::min<int32_t>(wl.ntiles(), sms * kCtasPerSm), 1);
+  add(ngrid, 4); add(1, 8);                                                             // deferred finish
   if (cudaMalloc(&b.mem, bytes) != cudaSuccess) return LARS_ERR_OOM;
   if (cudaMemset(b.mem, 0, bytes) != cudaSuccess) return LARS_ERR_CUDA;
   char* p = (char*)b.mem;
@@ -104,6 +106,8 @@ lars_status_t upload(DevBufs& b, int sms, int32_t nsplit_total, bool dp, int64_t
   b.sc.lambda = carve<double>(p, nt);
   b.sc.coef = carve<float>(p, nt);
   b.sc.beta = carve<float>(p, nt);
+  b.sc.nf_cta = carve<int32_t>(p, ngrid);
+  b.sc.step_iter = carve<int64_t>(p, 1);
   auto cp = [](void* d, const void* s, size_t n) { return n == 0 || cudaMemcpy(d, s, n, cudaMemcpyHostToDevice) == cudaSuccess; };
   std::vector<SegInfo> si(wl.segs.size());
   for (size_t k = 0; k < wl.segs.size(); ++k) {
@@ -194,6 +198,7 @@ struct lars_ctx {
     bool bulk = false;
   } fused;
   bool k1_bulk = false;     // Hyper::k1_bulk (LARS_K1_BULK)
+  bool defer = kDeferDefault;  // Hyper::defer for lars_step (LARS_DEFER_FINISH)
   int32_t k2_prefetch = 0;  // Hyper::k2_prefetch (LARS_K2_PREFETCH)
   bool k2_prefetch_g = false;
   int32_t last_red_dtype = LARS_F16;
@@ -391,6 +396,7 @@ lars_status_t lars_init(const lars_tensor_t* tensors, int32_t n, const lars_hpar
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0) h->sms = sms;
     // K1 through bulk-copy stages when its shared memory still leaves kCtasPerSm CTAs resident per SM
     // (the work list has one tile per resident CTA); LARS_K1_BULK=0/1 overrides (A/B measurement)
+    if (const char* df = getenv("LARS_DEFER_FINISH")) h->defer = df[0] == '1';
     const char* kb = getenv("LARS_K1_BULK");
     h->k1_bulk = kb ? kb[0] == '1' : kK1BulkDefault;
     if (h->k1_bulk &&
@@ -582,8 +588,10 @@ static lars_status_t carry_guard(lars_handle_t h, DevBufs& b, const float* w, cu
   return LARS_OK;
 }
 
-static lars_status_t step_impl(lars_handle_t h, float* w, const void* g, float* m, const Hyper& hy, void* stream) {
+static lars_status_t step_impl(lars_handle_t h, float* w, const void* g, float* m, const Hyper& hy_in, void* stream) {
   DeviceGuard dg(h->device);
+  Hyper hy = hy_in;
+  hy.defer = h->defer;  // the whole-layout step (no split layers): K2 finishes the layers
   cudaStream_t s = (cudaStream_t)stream;
   lars_status_t cg = carry_guard(h, h->full, w, s);
   if (cg != LARS_OK) return cg;

@@ -24,7 +24,9 @@ lars_status_t validate_hparams(const lars_hparams_t& hp) {
   if (!(fin(hp.eps) && hp.eps >= 0)) return LARS_ERR_INVALID_ARG;
   if (!(fin(hp.warmup_epochs) && hp.warmup_epochs >= 0)) return LARS_ERR_INVALID_ARG;
   if (!(fin(hp.poly_power) && hp.poly_power >= 0)) return LARS_ERR_INVALID_ARG;
-  if (!(fin(hp.grad_scale) && hp.grad_scale != 0)) return LARS_ERR_INVALID_ARG;
+  // |s| <= 2^64 keeps ||G|| = |s| sqrt(sum g^2) finite whenever the sum is (a sum of squares of <= 2^31 fp32
+  // values is < 2.5e86): a non-finite norm then means a non-finite partial sum (the deferred finish relies on it)
+  if (!(fin(hp.grad_scale) && hp.grad_scale != 0 && std::fabs(hp.grad_scale) <= 0x1p64)) return LARS_ERR_INVALID_ARG;
   if (hp.global_batch <= 0 || hp.dataset_size <= 0 || hp.total_epochs <= 0) return LARS_ERR_INVALID_ARG;
   if (hp.grad_dtype < LARS_F32 || hp.grad_dtype > LARS_BF16) return LARS_ERR_INVALID_ARG;
   if (hp.nranks < 1 || hp.nranks > 4096) return LARS_ERR_INVALID_ARG;

@@ -103,7 +103,7 @@ def test_error_codes():
         P.Lars([], device=-1, base_lr=1.0)
     assert e.value.status == 2  # empty layout
     for bad in (dict(base_lr=0.0), dict(base_lr=1.0, momentum=1.0), dict(base_lr=1.0, weight_decay=-1.0),
-                dict(base_lr=1.0, global_batch=0), dict(base_lr=float("nan")), dict(base_lr=1.0, grad_scale=0.0),
+                dict(base_lr=1.0, global_batch=0), dict(base_lr=float("nan")), dict(base_lr=1.0, grad_scale=0.0), dict(base_lr=1.0, grad_scale=2.0 ** 65),
                 dict(base_lr=1.0, warmup_epochs=1000.0), dict(base_lr=1.0, nranks=0)):
         with pytest.raises(P.LarsError) as e:
             P.Lars([(5, "weight")], device=-1, **bad)

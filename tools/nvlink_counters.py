@@ -29,6 +29,7 @@ class NvlinkCounters:
             sup = N.nvmlGpmQueryDeviceSupport(self.h)
             if getattr(sup, "isSupportedDevice", 0):
                 self.s1, self.s2 = N.nvmlGpmSampleAlloc(), N.nvmlGpmSampleAlloc()
+                N.nvmlGpmSampleGet(self.h, self.s1)  # answers NVML_ERROR_UNKNOWN on some pools: then no GPM
                 self.mode = "gpm"
         except Exception:  # noqa: BLE001 - evidence only
             self.mode = None
