@@ -303,7 +303,14 @@ def run_ours(args):
         h0 = mk(0)
         alt["no_carry_ms_per_step"] = time_loop(h0.lars_step, w, g)
         h0.close()
-        h.invalidate_carried_norms()  # w was advanced by another handle
+        # the paper's wire format at N = 1: fp16 gradients (18 B/param update), carried norms
+        hf = PK.Lars([(t.numel, t.kind) for t in lay], device=local, grad_dtype="f16", nranks=1,
+                     grad_scale=1.0 / G.GRAD_PRESCALE, flags=PK.lars.FLAG_CARRY_WNORM, **HP)
+        g16 = dev_flat(G.grads(lay, rank, 0, "f16"))
+        alt["f16_grad_ms_per_step"] = time_loop(hf.lars_step, w, g16)
+        hf.close()
+        del g16
+        h.invalidate_carried_norms()  # w was advanced by other handles
     if P > 1 and fused:
         alt["nccl_path_ms_per_step"] = time_loop(h.dp_allreduce_lars_step, w_n, g_n)
         # the NCCL path's phases, with reduce-scatter / all-gather bus bandwidth (nccl-tests convention:

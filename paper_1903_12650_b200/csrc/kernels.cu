@@ -1079,15 +1079,22 @@ __device__ __forceinline__ void k2_prefetch_first(const DevWork& wk, const Hyper
   }
 }
 
-// Deferred finish (single GPU, hy.defer), start of K2 after griddepcontrol.wait: K1 has left every
-// segment's partial sums, one non-finite flag per K1 CTA and (device iteration) the step's iteration.
+// Deferred finish (single GPU, hy.defer). K1 has left every segment's partial sums, one non-finite flag
+// per K1 CTA and (device iteration) the step's iteration. Before griddepcontrol.wait (while K1 drains) a
+// K2 CTA copies its tile's segment records (static work list) into shared memory; after the wait it reads
+// the flags and the partials of its tile's layers — one round of loads.
 // The step is skipped when any flag is set (a layer norm is non-finite exactly when one of its partials is:
 // the partials are sums of <= 2^31 fp32 squares and |s| <= 2^64, so no finite sum overflows the norm) or the
 // iteration is out of range; every CTA takes the same decision, CTA 0 records it and advances a device
 // iteration (every K1 CTA has read it; the next K1 reads it after this grid completes).
-__device__ __forceinline__ bool deferred_skip(const DevWork& wk, const DevScratch& sc, const Hyper& hy) {
-  int bad = 0;
-  for (int32_t i = threadIdx.x; i < wk.grid; i += blockDim.x) bad |= __ldcg(sc.nf_cta + i);
+__device__ __forceinline__ void deferred_prefetch_segs(int32_t tile, const DevWork& wk, SegInfo* sm_seg) {
+  const int32_t s0 = wk.tile_seg[tile], n = wk.tile_seg[tile + 1] - s0;
+  LARS_DCHECK(n >= 1 && n <= kMaxTileChunks);
+  for (int32_t i = threadIdx.x; i < 2 * n; i += blockDim.x)
+    cp_async16((char*)(sm_seg + i / 2) + 16 * (i & 1), (const char*)(wk.seginfo + s0 + i / 2) + 16 * (i & 1));
+}
+
+__device__ __forceinline__ bool deferred_skip(const DevWork& wk, const DevScratch& sc, const Hyper& hy, int bad) {
   bad = __syncthreads_or(bad);
   const int64_t t = hy.iter_dev ? __ldcg(sc.step_iter) : hy.iter;
   const bool in_range = t >= 0 && t < hy.total_iters;
@@ -1098,46 +1105,67 @@ __device__ __forceinline__ bool deferred_skip(const DevWork& wk, const DevScratc
   return bad || !in_range;
 }
 
-// The layers of `tile` (its segments s0..s1-1, one per layer, consecutive local tensor ids): each layer's
-// norms from ALL its segment partials in the same fixed order as K1's own finish (lane-strided sum, xor
-// butterfly: every CTA that touches the layer computes the same bits), then lambda and lr*lambda into the
-// CTA's shared arrays (index = tensor - base, base returned). The CTA holding a layer's first segment also
-// writes the layer's outputs (lars_last_norms).
+// The layers of `tile` (its segments, one per layer, consecutive local tensor ids; records in sm_seg): each
+// layer's norms from ALL its segment partials in the same fixed order as K1's own finish (lane-strided sum,
+// xor butterfly: every CTA that touches the layer computes the same bits), then lambda and lr*lambda into
+// the CTA's shared arrays (index = tensor - base, base returned). The CTA holding a layer's first segment
+// also writes the layer's outputs (lars_last_norms). `first`: also reduce the K1 flags into the skip decision
+// (their loads are issued beside the partials').
 __device__ __forceinline__ int32_t deferred_finish_tile(int32_t tile, const DevWork& wk, const DevScratch& sc,
-                                                        const Hyper& hy, float* sm_coef, float* sm_beta) {
+                                                        const Hyper& hy, const SegInfo* sm_seg, float* sm_coef,
+                                                        float* sm_beta, bool first, bool* skip) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int32_t s0 = wk.tile_seg[tile], s1 = wk.tile_seg[tile + 1];
-  const int32_t base = wk.seginfo[s0].tensor;
+  int bad = 0;
+  if (first)
+    for (int32_t i = threadIdx.x; i < wk.grid; i += blockDim.x) bad |= __ldcg(sc.nf_cta + i);
+  cp_async_wait_all();
+  __syncthreads();  // the tile's segment records are in shared memory
+  const int32_t base = sm_seg[0].tensor;
   const int64_t t = hy.iter_dev ? __ldcg(sc.step_iter) : hy.iter;
   const bool in_range = t >= 0 && t < hy.total_iters;
   const double lr = in_range ? hy.lr_table[t] : 0.0;
-  for (int32_t s = s0 + warp; s < s1; s += kThreads / 32) {
-    const SegInfo si = wk.seginfo[s];
-    LARS_DCHECK(si.tensor - base == s - s0 && si.tensor - base < kMaxTileChunks);
-    double sw, sg;
-    warp_sum2(sc.part_w, sc.part_g, si.tseg_begin, si.tseg_begin + si.nseg, lane, sw, sg);
-    if (lane == 0) {
-      const double wn = sqrt(sw), gn = fabs(hy.grad_scale) * sqrt(sg);
-      double lam = 1.0, beta = 0.0;
-      if (si.lars) {  // reading #1, #3, #4 (same arithmetic as finish_core)
-        beta = hy.weight_decay;
-        const double den = gn + hy.weight_decay * wn + hy.eps;
-        if (wn > 0.0 && den > hy.eps) lam = hy.eta * wn / den;
-      }
-      const float cf = in_range ? (float)(lr * lam) : 0.0f;
-      sm_coef[s - s0] = cf;
-      sm_beta[s - s0] = (float)beta;
-      if (s == si.tseg_begin) {
-        const int32_t l = si.tensor;
-        sc.w_norm[l] = wn;
-        sc.g_norm[l] = gn;
-        sc.lambda[l] = lam;
-        sc.coef[l] = cf;
-        sc.beta[l] = (float)beta;
-      }
+  const int32_t n = s1 - s0;
+  auto finish = [&](int32_t k, const SegInfo& si, double sw, double sg) {
+    const double wn = sqrt(sw), gn = fabs(hy.grad_scale) * sqrt(sg);
+    double lam = 1.0, beta = 0.0;
+    if (si.lars) {  // reading #1, #3, #4 (same arithmetic as finish_core)
+      beta = hy.weight_decay;
+      const double den = gn + hy.weight_decay * wn + hy.eps;
+      if (wn > 0.0 && den > hy.eps) lam = hy.eta * wn / den;
+    }
+    const float cf = in_range ? (float)(lr * lam) : 0.0f;
+    sm_coef[k] = cf;
+    sm_beta[k] = (float)beta;
+    if (s0 + k == si.tseg_begin) {
+      const int32_t l = si.tensor;
+      sc.w_norm[l] = wn;
+      sc.g_norm[l] = gn;
+      sc.lambda[l] = lam;
+      sc.coef[l] = cf;
+      sc.beta[l] = (float)beta;
+    }
+  };
+  // A tile's interior segments are whole layers (one partial each): one thread per layer, all loads at once.
+  for (int32_t k = threadIdx.x; k < n; k += blockDim.x) {
+    const SegInfo si = sm_seg[k];
+    LARS_DCHECK(si.tensor - base == k && k < kMaxTileChunks);
+    LARS_DCHECK(si.nseg == 1 || k == 0 || k == n - 1);
+    if (si.nseg == 1) finish(k, si, __ldcg(sc.part_w + si.tseg_begin), __ldcg(sc.part_g + si.tseg_begin));
+  }
+  // Only the first and the last segment can belong to a layer spread over several tiles: warps 0 and 1 sum
+  // those layers' partials (the fixed order of K1's own finish).
+  if (warp < 2 && (warp == 0 || n > 1)) {
+    const int32_t k = warp == 0 ? 0 : n - 1;
+    const SegInfo si = sm_seg[k];
+    if (si.nseg > 1) {
+      double sw, sg;
+      warp_sum2(sc.part_w, sc.part_g, si.tseg_begin, si.tseg_begin + si.nseg, lane, sw, sg);
+      if (lane == 0) finish(k, si, sw, sg);
     }
   }
-  __syncthreads();
+  if (first) *skip = deferred_skip(wk, sc, hy, bad);  // (its __syncthreads_or also publishes sm_coef)
+  else __syncthreads();
   return base;
 }
 
@@ -1152,14 +1180,17 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_update_kernel(DevWo
   pdl_trigger();
   // K1 writes none of w, g, m: while K1 drains, pull the first chunks this CTA updates into L2
   if (hy.k2_prefetch > 0) k2_prefetch_first<DT>(wk, hy, w, g, g_shift, m);
+  __shared__ __align__(16) SegInfo sm_seg[HALF ? 1 : kMaxTileChunks];  // deferred finish: the tile's segments
+  if (!HALF && hy.defer && blockIdx.x < wk.ntiles) deferred_prefetch_segs(blockIdx.x, wk, sm_seg);
   pdl_wait();
-  bool skip;
+  bool skip = false;
   TRACE_BEGIN
   if (!HALF && hy.defer) {
-    skip = deferred_skip(wk, sc, hy);
     for (int32_t tile = blockIdx.x; tile < wk.ntiles; tile += gridDim.x) {
       __shared__ float sm_coef[kMaxTileChunks], sm_beta[kMaxTileChunks];
-      const int32_t base = deferred_finish_tile(tile, wk, sc, hy, sm_coef, sm_beta);
+      const bool first = tile == (int32_t)blockIdx.x;
+      if (!first) deferred_prefetch_segs(tile, wk, sm_seg);
+      const int32_t base = deferred_finish_tile(tile, wk, sc, hy, sm_seg, sm_coef, sm_beta, first, &skip);
       if (!skip)
         for (int32_t q = kUpdateSplit - 1; q >= 0; --q)
           update_item<DT, CARRY>((kUpdateSplit - 1 - q) * wk.ntiles + tile, wk, sc, hy, w, g, g_shift, m, NoPeers(),

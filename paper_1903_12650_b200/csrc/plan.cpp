@@ -369,6 +369,15 @@ const char* check_worklist(const Plan& p, const WorkList& wl, int32_t rank) {
     if (ns > 0 && wl.tile_seg[t + 1] <= wl.tile_seg[t]) return "a tile without segments";
     if (wl.tile_chunk[t] != wl.seg_chunk[wl.tile_seg[t]]) return "tile_chunk inconsistent with seg_chunk";
     if (wl.tile_chunk[t + 1] - wl.tile_chunk[t] > kMaxTileChunks) return "tile exceeds kMaxTileChunks chunks";
+    // K2's deferred finish: a tile's segments are consecutive local tensors, and only its first and last
+    // segment may belong to a tensor spread over several tiles
+    for (int32_t s = wl.tile_seg[t]; s < wl.tile_seg[t + 1]; ++s) {
+      const int32_t li = wl.segs[s].tensor;
+      if (s > wl.tile_seg[t] && li != wl.segs[s - 1].tensor + 1) return "a tile's tensors are not consecutive";
+      if (li >= 0 && li < (int32_t)wl.tseg_count.size() && wl.tseg_count[li] > 1 && s != wl.tile_seg[t] &&
+          s != wl.tile_seg[t + 1] - 1)
+        return "a multi-tile tensor inside a tile";
+    }
   }
   if ((int32_t)wl.seg_chunk.size() != ns + 1 || wl.seg_chunk.front() != 0 || wl.seg_chunk.back() != nc)
     return "seg_chunk does not span the chunks";

@@ -299,3 +299,43 @@ def test_variants_step_decay_and_momentum_form(dtype, form):
         s.step(t)
         r, _ = s.check(t, pre_w, [g], pre_m, TOL_F32, tag=f"{form} {dtype} t={t}")
         assert r.lr == s.h.lr_at(t) and r.lr == (32.0 if t < 480 else 32.0 * 0.1)
+
+
+@pytest.mark.parametrize("layout", ["resnet50", "skew"])
+def test_deferred_finish_matches_k1_finish(layout, monkeypatch):
+    """The layer finish in K2's prologue (default for lars_step) and the finish in K1's tail
+    (LARS_DEFER_FINISH=0) sum the same segment partials in the same fixed order: bitwise-equal w, m, norms,
+    lambda and coefficients, over applied steps, carried norms, a device-iteration graph step at the end of
+    the schedule and a skipped (NaN) step."""
+    torch = _torch()
+    import paper_1903_12650_b200 as PK
+
+    rng = np.random.default_rng(77)
+    lay = LY.resnet50() if layout == "resnet50" else LY.random_layout(rng, 40, max_numel=300000)
+    runs = []
+    for defer in ("1", "0"):
+        monkeypatch.setenv("LARS_DEFER_FINISH", defer)
+        s = GpuStep(lay, grad_dtype="f16", flags=PK.lars.FLAG_CARRY_WNORM)
+        s.upload(G.weights(lay), G.grads(lay, 0, 5, "f16"), G.momentum(lay, 1e-3))
+        out = []
+        for t in (79, 80, 700):
+            s.step(t)
+            out.append(s.h.last_norms())
+        it = torch.tensor([1439], dtype=torch.int64, device=s.w.device)
+        s.h.lars_step_dev_iter(s.w, s.g, s.m, it)
+        torch.cuda.synchronize()
+        assert int(it.item()) == 1440 and not s.h.last_step_skipped()
+        s.h.lars_step_dev_iter(s.w, s.g, s.m, it)  # t = T: out of range -> status 2, untouched
+        torch.cuda.synchronize()
+        assert s.h.last_step_status() == 2
+        s.g.view(torch.float16)[s.h.offsets[len(lay) // 2]] = float("nan")
+        s.step(701)
+        torch.cuda.synchronize()
+        assert s.h.last_step_skipped()
+        runs.append((s.w.clone(), s.m.clone(), out))
+        s.h.close()
+    (wa, ma, na), (wb, mb, nb) = runs
+    assert torch.equal(wa, wb) and torch.equal(ma, mb)
+    for x, y in zip(na, nb):
+        for u, v in zip(x, y):
+            assert np.array_equal(np.asarray(u), np.asarray(v))
