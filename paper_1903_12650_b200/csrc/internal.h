@@ -183,6 +183,7 @@ struct Hyper {
   bool k2_prefetch_g = false;  // ... and their gradient
   bool k1_bulk = false;      // K1 streams its chunks through the bulk-copy engine (stream_tile_bulk)
   bool defer = false;        // single GPU: the layer finish moves from K1's tail into K2's prologue
+  double lr_host = 0.0;      // lr(iter) from the host's table (host-given iteration; saves K2 a load)
 };
 
 // g_shift: the gradient of flat element e is g[e - g_shift] (the DP step reads its reduced shard).

@@ -391,7 +391,20 @@ __device__ __forceinline__ void acc4(double& a, const float4& x) {
 __device__ __forceinline__ void warp_sum2(const double* xa, const double* xb, int32_t a, int32_t b, int lane,
                                           double& ra, double& rb) {
   double sa = 0.0, sb = 0.0;
-  for (int32_t i = a + lane; i < b; i += 32) {
+  int32_t i = a + lane;
+  for (; i + 96 < b; i += 128) {  // four loads of each in flight, added in the same order as one at a time
+    const double a0 = __ldcg(xa + i), a1 = __ldcg(xa + i + 32), a2 = __ldcg(xa + i + 64), a3 = __ldcg(xa + i + 96);
+    const double b0 = __ldcg(xb + i), b1 = __ldcg(xb + i + 32), b2 = __ldcg(xb + i + 64), b3 = __ldcg(xb + i + 96);
+    sa += a0;
+    sa += a1;
+    sa += a2;
+    sa += a3;
+    sb += b0;
+    sb += b1;
+    sb += b2;
+    sb += b3;
+  }
+  for (; i < b; i += 32) {
     sa += __ldcg(xa + i);
     sb += __ldcg(xb + i);
   }
@@ -969,28 +982,28 @@ struct McastWeights {
 // One warp chunk of K2 (and F2): unscale + weight decay + momentum + update of <= kChunk elements, every new
 // weight also handed to `ws` (the other ranks' buffers on the fused path); carry mode also leaves the chunk's
 // sum(w_new^2) for the next step's K1.
-// Per-layer coefficients K2 reads: lr*lambda and beta_l of local tensor l at coef[l - base], beta[l - base]
-// (the scratch arrays, base 0; or, deferred finish, the CTA's shared copies for its tile's layers).
-struct Coefs {
-  const float* coef;
-  const float* beta;
-  int32_t base;
-};
+// Deferred finish (K2 prologue): the coefficients of the layers of the CTA's current tile, indexed by
+// local tensor id - base, and the tile's segment records.
+__shared__ float k2_coef[kMaxTileChunks], k2_beta[kMaxTileChunks];
+__shared__ __align__(16) SegInfo k2_seg[kMaxTileChunks];
 
-template <int DT, bool CARRY, typename WS = NoPeers>
+// DEFER: lr*lambda and beta_l come from the CTA's shared copies (k2_coef/k2_beta, index tensor - base),
+// otherwise from the scratch arrays K1 (or the split finisher) wrote.
+template <int DT, bool CARRY, typename WS = NoPeers, bool DEFER = false>
 __device__ __forceinline__ void update_chunk(int32_t c, const DevWork& wk, const DevScratch& sc, const Hyper& hy,
                                              float* __restrict__ w, const void* __restrict__ g, int64_t g_shift,
-                                             float* __restrict__ m, const WS& ws, const Coefs& cs) {
+                                             float* __restrict__ m, const WS& ws, int32_t base) {
   const int lane = threadIdx.x & 31;
   const float s = hy.grad_scale_f, mu = hy.mu;
   const Seg ck = wk.chunks[c];
   check_chunk(wk, c, ck);
-  const float cf = cs.coef[ck.tensor - cs.base], b = cs.beta[ck.tensor - cs.base];
+  const float cf = DEFER ? k2_coef[ck.tensor - base] : sc.coef[ck.tensor];
+  const float b = DEFER ? k2_beta[ck.tensor - base] : sc.beta[ck.tensor];
   float* wp = w + ck.begin;
   float* mp = m + ck.begin;
   const int64_t gi = ck.begin - g_shift;
   const int32_t ng = ck.len >> 3;
-  double aw = 0.0, aw1 = 0.0;  // CARRY: sum(w_new^2) of this chunk for the next step's K1
+  double aw = 0.0;  // CARRY: sum(w_new^2) of this chunk for the next step's K1
   for (int32_t i = (ng << 3) + lane; i < ck.len; i += 32) {  // ragged tensor tail (< 8 elements)
     const float wv = wp[i], mv = mp[i];
     const float u = fmaf(b, wv, s * Grad<DT>::load1(g, gi + i));
@@ -1015,9 +1028,9 @@ __device__ __forceinline__ void update_chunk(int32_t c, const DevWork& wk, const
     st8(mp + 8 * j1, m1);
     ws.store8(ck.begin + 8 * j, w0);
     ws.store8(ck.begin + 8 * j1, w1);
-    if (CARRY) {
+    if (CARRY) {  // one fp64 accumulator (a second one for ILP cost spills at the 64-register budget)
       accw8(aw, w0);
-      accw8(aw1, w1);
+      accw8(aw, w1);
     }
   }
   if (j >= 0) {
@@ -1030,18 +1043,16 @@ __device__ __forceinline__ void update_chunk(int32_t c, const DevWork& wk, const
     if (CARRY) accw8(aw, w0);
   }
   if (CARRY) {
-    aw += aw1;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) aw += __shfl_xor_sync(0xffffffffu, aw, o);
     if (lane == 0) sc.cpart_wnext[c] = aw;
   }
 }
 
-template <int DT, bool CARRY, typename WS = NoPeers>
+template <int DT, bool CARRY, typename WS = NoPeers, bool DEFER = false>
 __device__ __forceinline__ void update_item(int32_t item, const DevWork& wk, const DevScratch& sc, const Hyper& hy,
                                             float* __restrict__ w, const void* __restrict__ g, int64_t g_shift,
-                                            float* __restrict__ m, const WS& ws = WS(), Coefs cs = Coefs{}) {
-  if (!cs.coef) cs = Coefs{sc.coef, sc.beta, 0};
+                                            float* __restrict__ m, const WS& ws = WS(), int32_t base = 0) {
   constexpr int kWarps = kThreads / 32;
   const int warp = threadIdx.x >> 5;
   // item -> (part q, tile): all tiles' last parts first (the bytes K1 read last, still in L2), then the
@@ -1052,7 +1063,7 @@ __device__ __forceinline__ void update_item(int32_t item, const DevWork& wk, con
   const int32_t c1 = t0 + (int32_t)((int64_t)tn * (q + 1) / kUpdateSplit);
   LARS_DCHECK(tile >= 0 && tile < wk.ntiles && q >= 0 && q < kUpdateSplit && c0 <= c1 && c1 <= wk.nchunks);
   for (int32_t c = c1 - 1 - warp; c >= c0; c -= kWarps)  // backwards: K1's most recent reads first
-    update_chunk<DT, CARRY, WS>(c, wk, sc, hy, w, g, g_shift, m, ws, cs);
+    update_chunk<DT, CARRY, WS, DEFER>(c, wk, sc, hy, w, g, g_shift, m, ws, base);
 }
 
 // Before K2's griddepcontrol.wait (its CTAs become resident as K1's retire): the bulk-copy engine
@@ -1087,7 +1098,8 @@ __device__ __forceinline__ void k2_prefetch_first(const DevWork& wk, const Hyper
 // the partials are sums of <= 2^31 fp32 squares and |s| <= 2^64, so no finite sum overflows the norm) or the
 // iteration is out of range; every CTA takes the same decision, CTA 0 records it and advances a device
 // iteration (every K1 CTA has read it; the next K1 reads it after this grid completes).
-__device__ __forceinline__ void deferred_prefetch_segs(int32_t tile, const DevWork& wk, SegInfo* sm_seg) {
+__device__ __forceinline__ void deferred_prefetch_segs(int32_t tile, const DevWork& wk) {
+  SegInfo* sm_seg = k2_seg;
   const int32_t s0 = wk.tile_seg[tile], n = wk.tile_seg[tile + 1] - s0;
   LARS_DCHECK(n >= 1 && n <= kMaxTileChunks);
   for (int32_t i = threadIdx.x; i < 2 * n; i += blockDim.x)
@@ -1112,19 +1124,31 @@ __device__ __forceinline__ bool deferred_skip(const DevWork& wk, const DevScratc
 // also writes the layer's outputs (lars_last_norms). `first`: also reduce the K1 flags into the skip decision
 // (their loads are issued beside the partials').
 __device__ __forceinline__ int32_t deferred_finish_tile(int32_t tile, const DevWork& wk, const DevScratch& sc,
-                                                        const Hyper& hy, const SegInfo* sm_seg, float* sm_coef,
-                                                        float* sm_beta, bool first, bool* skip) {
+                                                        const Hyper& hy, bool first, bool* skip) {
+  const SegInfo* sm_seg = k2_seg;
+  float* sm_coef = k2_coef;
+  float* sm_beta = k2_beta;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int32_t s0 = wk.tile_seg[tile], s1 = wk.tile_seg[tile + 1];
-  int bad = 0;
-  if (first)
-    for (int32_t i = threadIdx.x; i < wk.grid; i += blockDim.x) bad |= __ldcg(sc.nf_cta + i);
-  cp_async_wait_all();
-  __syncthreads();  // the tile's segment records are in shared memory
-  const int32_t base = sm_seg[0].tensor;
+  // every load of the prologue is issued before any of them is used: the K1 flags (first tile; OR-ed at
+  // the end), the iteration, then — once the segment records are in — the partials
+  int f0 = 0, f1 = 0, f2 = 0;
+  if (first) {
+    const int32_t i = threadIdx.x;
+    if (i < wk.grid) f0 = __ldcg(sc.nf_cta + i);
+    if (i + kThreads < wk.grid) f1 = __ldcg(sc.nf_cta + i + kThreads);
+    if (i + 2 * kThreads < wk.grid) f2 = __ldcg(sc.nf_cta + i + 2 * kThreads);
+    for (int32_t j = i + 3 * kThreads; j < wk.grid; j += kThreads) f2 |= __ldcg(sc.nf_cta + j);
+  }
   const int64_t t = hy.iter_dev ? __ldcg(sc.step_iter) : hy.iter;
   const bool in_range = t >= 0 && t < hy.total_iters;
-  const double lr = in_range ? hy.lr_table[t] : 0.0;
+  const double lr = !in_range ? 0.0 : hy.iter_dev ? hy.lr_table[t] : hy.lr_host;
+  cp_async_wait_all();
+  __syncthreads();  // the tile's segment records are in shared memory
+  if (first) {
+    TRACE_MARK_AT(5, 1)
+  }
+  const int32_t base = sm_seg[0].tensor;
   const int32_t n = s1 - s0;
   auto finish = [&](int32_t k, const SegInfo& si, double sw, double sg) {
     const double wn = sqrt(sw), gn = fabs(hy.grad_scale) * sqrt(sg);
@@ -1153,10 +1177,15 @@ __device__ __forceinline__ int32_t deferred_finish_tile(int32_t tile, const DevW
     LARS_DCHECK(si.nseg == 1 || k == 0 || k == n - 1);
     if (si.nseg == 1) finish(k, si, __ldcg(sc.part_w + si.tseg_begin), __ldcg(sc.part_g + si.tseg_begin));
   }
-  // Only the first and the last segment can belong to a layer spread over several tiles: warps 0 and 1 sum
-  // those layers' partials (the fixed order of K1's own finish).
-  if (warp < 2 && (warp == 0 || n > 1)) {
-    const int32_t k = warp == 0 ? 0 : n - 1;
+  if (first) {
+    TRACE_MARK_AT(5, 2)
+  }
+  // Only the first and the last segment can belong to a layer spread over several tiles: the two last warps
+  // (idle in the pass above unless the tile has > 192 layers) sum those layers' partials (the fixed order
+  // of K1's own finish).
+  constexpr int kW0 = kThreads / 32 - 2;
+  if (warp >= kW0 && (warp == kW0 || n > 1)) {
+    const int32_t k = warp == kW0 ? 0 : n - 1;
     const SegInfo si = sm_seg[k];
     if (si.nseg > 1) {
       double sw, sg;
@@ -1164,7 +1193,7 @@ __device__ __forceinline__ int32_t deferred_finish_tile(int32_t tile, const DevW
       if (lane == 0) finish(k, si, sw, sg);
     }
   }
-  if (first) *skip = deferred_skip(wk, sc, hy, bad);  // (its __syncthreads_or also publishes sm_coef)
+  if (first) *skip = deferred_skip(wk, sc, hy, f0 | f1 | f2);  // (its __syncthreads_or also publishes sm_coef)
   else __syncthreads();
   return base;
 }
@@ -1172,29 +1201,31 @@ __device__ __forceinline__ int32_t deferred_finish_tile(int32_t tile, const DevW
 // K2. Same persistent schedule as K1 (CTA b owns tiles b, b + grid, ...; identical grid and resources,
 // so CTA b runs on the same SM in both kernels) and each tile's chunks walked backwards: the gradient
 // bytes K1 streamed last into this SM's L2 slice are re-read first.
-template <int DT, bool CARRY, bool HALF = false>
+template <int DT, bool CARRY, bool HALF = false, bool DEFER = false>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_update_kernel(DevWork wk, DevScratch sc, Hyper hy,
                                                                            float* __restrict__ w,
                                                                            const void* __restrict__ g,
                                                                            int64_t g_shift, float* __restrict__ m) {
+  static_assert(!(HALF && DEFER), "the deferred finish is the whole-layout step's");
   pdl_trigger();
   // K1 writes none of w, g, m: while K1 drains, pull the first chunks this CTA updates into L2
   if (hy.k2_prefetch > 0) k2_prefetch_first<DT>(wk, hy, w, g, g_shift, m);
-  __shared__ __align__(16) SegInfo sm_seg[HALF ? 1 : kMaxTileChunks];  // deferred finish: the tile's segments
-  if (!HALF && hy.defer && blockIdx.x < wk.ntiles) deferred_prefetch_segs(blockIdx.x, wk, sm_seg);
+  if constexpr (DEFER) deferred_prefetch_segs(blockIdx.x, wk);  // static work list: before the wait
   pdl_wait();
   bool skip = false;
   TRACE_BEGIN
-  if (!HALF && hy.defer) {
+  if constexpr (DEFER) {
     for (int32_t tile = blockIdx.x; tile < wk.ntiles; tile += gridDim.x) {
-      __shared__ float sm_coef[kMaxTileChunks], sm_beta[kMaxTileChunks];
       const bool first = tile == (int32_t)blockIdx.x;
-      if (!first) deferred_prefetch_segs(tile, wk, sm_seg);
-      const int32_t base = deferred_finish_tile(tile, wk, sc, hy, sm_seg, sm_coef, sm_beta, first, &skip);
+      if (!first) deferred_prefetch_segs(tile, wk);
+      const int32_t base = deferred_finish_tile(tile, wk, sc, hy, first, &skip);
+      if (first) {
+        TRACE_MARK_AT(5, 0)  // (diagnostics build) prologue done
+      }
       if (!skip)
         for (int32_t q = kUpdateSplit - 1; q >= 0; --q)
-          update_item<DT, CARRY>((kUpdateSplit - 1 - q) * wk.ntiles + tile, wk, sc, hy, w, g, g_shift, m, NoPeers(),
-                                 Coefs{sm_coef, sm_beta, base});
+          update_item<DT, CARRY, NoPeers, true>((kUpdateSplit - 1 - q) * wk.ntiles + tile, wk, sc, hy, w, g, g_shift,
+                                                m, NoPeers(), base);
       __syncthreads();  // the tile's coefficients are consumed before the next tile's overwrite them
     }
   } else {
@@ -1659,6 +1690,10 @@ static cudaError_t launch_update_t(const DevWork& wk, const DevScratch& sc, cons
       if (hy.carry) return launch_pdl(lars_update_kernel<DT, true, true>, wk.grid, st, wk, sc, hy, w, g, g_shift, m);
       return launch_pdl(lars_update_kernel<DT, false, true>, wk.grid, st, wk, sc, hy, w, g, g_shift, m);
     }
+  }
+  if (hy.defer) {
+    if (hy.carry) return launch_pdl(lars_update_kernel<DT, true, false, true>, wk.grid, st, wk, sc, hy, w, g, g_shift, m);
+    return launch_pdl(lars_update_kernel<DT, false, false, true>, wk.grid, st, wk, sc, hy, w, g, g_shift, m);
   }
   if (hy.carry) return launch_pdl(lars_update_kernel<DT, true>, wk.grid, st, wk, sc, hy, w, g, g_shift, m);
   return launch_pdl(lars_update_kernel<DT, false>, wk.grid, st, wk, sc, hy, w, g, g_shift, m);

@@ -573,6 +573,7 @@ static Hyper hyper(lars_handle_t h, int64_t iter, int64_t* iter_dev = nullptr) {
            (h->hp.flags & LARS_FLAG_LR_AT_APPLY) != 0};
   hy.k2_prefetch = h->k2_prefetch;
   hy.k1_bulk = h->k1_bulk;
+  if (!iter_dev && iter >= 0 && iter < (int64_t)h->plan.lr.size()) hy.lr_host = h->plan.lr[iter];
   hy.k2_prefetch_g = h->k2_prefetch_g;
   return hy;
 }

@@ -17,3 +17,8 @@ echo "ncu full rc=$?"
 ncu --cache-control none --clock-control none --metrics dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct,gpu__time_duration.sum \
     -k regex:lars_ -s 6 -c 4 --csv python tools/profile_step.py --flags 1 > gpurun_out/ncu_warm_${TAG}.csv 2>&1
 echo "ncu warm rc=$?"
+# configs[3] and configs[4] at P = 1 with the round's code (no profiler)
+timeout 600 python tools/schedule_replay.py > gpurun_out/r152_replay_${TAG}.jsonl 2> gpurun_out/r152_replay_${TAG}.err
+echo "schedule_replay rc=$?"
+timeout 900 python tools/skew_sweep.py > gpurun_out/skew_sweep_${TAG}.jsonl 2> gpurun_out/skew_sweep_${TAG}.err
+echo "skew_sweep rc=$?"

@@ -49,6 +49,13 @@ def main():
     t0k1 = tr[0, :n1, 0].min()
     pa = (tr[4, :n1, 0] - t0k1) / 1e3
     print(f"K1 phase A (chunk streaming) done: min/p50/max = {pa.min():.1f}/{np.median(pa):.1f}/{pa.max():.1f} us")
+    n2 = int(tr[1, 0, 3])
+    pro = (tr[5, :n2, 0] - tr[1, :n2, 0]) / 1e3
+    if (tr[5, :n2, 0] > 0).all():
+        print(f"K2 deferred-finish prologue: min/p50/max = {pro.min():.2f}/{np.median(pro):.2f}/{pro.max():.2f} us")
+        for k, what in ((1, "segment records + flags in"), (2, "whole layers finished")):
+            x = (tr[5, :n2, k] - tr[1, :n2, 0]) / 1e3
+            print(f"  {what}: min/p50/max = {x.min():.2f}/{np.median(x):.2f}/{x.max():.2f} us")
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     np.save(os.path.join(ROOT, "gpurun_out", "trace_step.npy"), tr)
     for k, name in enumerate(["K1 norms", "K2 update"]):
