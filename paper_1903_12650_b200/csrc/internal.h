@@ -42,7 +42,6 @@ constexpr int32_t kUpdateSplit = 4;     // K2 walks each tile in 4 parts, last p
 constexpr int kNormUnroll = LARS_NORM_UNROLL;  // K1 vector groups per lane per iteration
 constexpr int32_t kDefaultMinTile = 4096;
 constexpr bool kK1BulkDefault = false;  // K1 bulk-copy streaming (Hyper::k1_bulk) unless LARS_K1_BULK says
-constexpr bool kDpBulkDefault = false;  // F1 bulk-copy streaming (DpFused::bulk) unless LARS_DP_BULK says
 constexpr bool kDeferDefault = true;  // lars_step: layer finish in K2's prologue unless LARS_DEFER_FINISH=0
 constexpr int32_t kChunk = 2048;        // elements per warp work item (multiple of 256)
 

@@ -836,18 +836,21 @@ __device__ __forceinline__ bool norms_body(const DevWork& wk, const DevScratch& 
   return false;
 }
 
-template <int DT, bool CARRY>
+// BULK: a separate instance streaming through bulk-copy stages (its shared-memory attributes — 48 KB of
+// dynamic stages, the max-shared carveout — must not touch the register-loop instance, which runs faster
+// with the default L1/shared split).
+template <int DT, bool CARRY, bool BULK = false>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_norms_kernel(DevWork wk, DevScratch sc, Hyper hy,
                                                                           const float* __restrict__ w,
                                                                           const void* __restrict__ g,
                                                                           int64_t g_shift) {
   // wait BEFORE releasing the dependent K2: K2 prefetches w and m before its own wait, so it must not
   // become resident while the previous step's K2 may still be writing them
-  extern __shared__ __align__(128) unsigned char k1_stages[];  // kBulkSmem bytes when hy.k1_bulk
+  extern __shared__ __align__(128) unsigned char k1_stages[];  // kBulkSmem bytes when BULK
   pdl_wait();
   pdl_trigger();
   TRACE_BEGIN
-  norms_body<CARRY>(wk, sc, hy, w, LocalGrad<DT>{g, g_shift}, hy.k1_bulk ? k1_stages : nullptr);
+  norms_body<CARRY, LocalGrad<DT>, !BULK>(wk, sc, hy, w, LocalGrad<DT>{g, g_shift}, BULK ? k1_stages : nullptr);
   TRACE_END(0)
 }
 
@@ -1504,11 +1507,24 @@ static void launch_reduce_norms_np(int np, int grid, cudaStream_t st, const DevW
     launch_pdl_smem(lars_dp_reduce_norms_kernel<DT, CARRY, 8, BULK>, grid, st, true, smem, wk, sc, hy, w, f);
 }
 
+// Bulk-copy instances: static + dynamic shared memory exceeds the 48 KB a kernel gets without opting in,
+// and 4 CTAs x ~53 KB per SM need the largest shared-memory carveout.
+template <typename K>
+static void prefer_shared(K kernel) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem);
+  cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+}
+
 template <int DT, bool CARRY, bool BULK>
 static int reduce_norms_occupancy_np(int np) {
   int n = 0;
   cudaError_t e;
   const size_t smem = BULK ? kBulkSmem : 0;
+  if (BULK) {
+    prefer_shared(lars_dp_reduce_norms_kernel<DT, CARRY, 2, BULK>);
+    prefer_shared(lars_dp_reduce_norms_kernel<DT, CARRY, 4, BULK>);
+    prefer_shared(lars_dp_reduce_norms_kernel<DT, CARRY, 8, BULK>);
+  }
   if (np <= 2)
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lars_dp_reduce_norms_kernel<DT, CARRY, 2, BULK>, kThreads, smem);
   else if (np <= 4)
@@ -1661,26 +1677,27 @@ cudaError_t launch_init_weights(const DevWork& wk, const InitTable& it, float* w
 template <int DT>
 static cudaError_t launch_norms_t(const DevWork& wk, const DevScratch& sc, const Hyper& hy, const float* w,
                                   const void* g, int64_t g_shift, cudaStream_t st) {
-  const size_t smem = hy.k1_bulk ? kBulkSmem : 0;
-  if (hy.carry) return launch_pdl_smem(lars_norms_kernel<DT, true>, wk.grid, st, false, smem, wk, sc, hy, w, g, g_shift);
-  return launch_pdl_smem(lars_norms_kernel<DT, false>, wk.grid, st, false, smem, wk, sc, hy, w, g, g_shift);
+  if (hy.k1_bulk) {
+    if (hy.carry)
+      return launch_pdl_smem(lars_norms_kernel<DT, true, true>, wk.grid, st, false, kBulkSmem, wk, sc, hy, w, g, g_shift);
+    return launch_pdl_smem(lars_norms_kernel<DT, false, true>, wk.grid, st, false, kBulkSmem, wk, sc, hy, w, g, g_shift);
+  }
+  if (hy.carry) return launch_pdl(lars_norms_kernel<DT, true>, wk.grid, st, wk, sc, hy, w, g, g_shift);
+  return launch_pdl(lars_norms_kernel<DT, false>, wk.grid, st, wk, sc, hy, w, g, g_shift);
 }
 
 // Resident K1 CTAs per SM with the bulk-copy stages (the work list assumes kCtasPerSm).
-int norms_bulk_blocks_per_sm(int32_t dt, bool carry) {
+template <int DT, bool CARRY>
+static int norms_bulk_occupancy() {
   int n = 0;
-  cudaError_t e;
-  const size_t smem = kBulkSmem;
-  if (dt == LARS_F32)
-    e = carry ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lars_norms_kernel<LARS_F32, true>, kThreads, smem)
-              : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lars_norms_kernel<LARS_F32, false>, kThreads, smem);
-  else if (dt == LARS_F16)
-    e = carry ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lars_norms_kernel<LARS_F16, true>, kThreads, smem)
-              : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lars_norms_kernel<LARS_F16, false>, kThreads, smem);
-  else
-    e = carry ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lars_norms_kernel<LARS_BF16, true>, kThreads, smem)
-              : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lars_norms_kernel<LARS_BF16, false>, kThreads, smem);
-  return e == cudaSuccess ? n : 0;
+  prefer_shared(lars_norms_kernel<DT, CARRY, true>);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, lars_norms_kernel<DT, CARRY, true>, kThreads, kBulkSmem) ==
+                 cudaSuccess ? n : 0;
+}
+int norms_bulk_blocks_per_sm(int32_t dt, bool carry) {
+  if (dt == LARS_F32) return carry ? norms_bulk_occupancy<LARS_F32, true>() : norms_bulk_occupancy<LARS_F32, false>();
+  if (dt == LARS_F16) return carry ? norms_bulk_occupancy<LARS_F16, true>() : norms_bulk_occupancy<LARS_F16, false>();
+  return carry ? norms_bulk_occupancy<LARS_BF16, true>() : norms_bulk_occupancy<LARS_BF16, false>();
 }
 template <int DT>
 static cudaError_t launch_update_t(const DevWork& wk, const DevScratch& sc, const Hyper& hy, float* w,

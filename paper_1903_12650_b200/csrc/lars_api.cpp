@@ -399,9 +399,11 @@ lars_status_t lars_init(const lars_tensor_t* tensors, int32_t n, const lars_hpar
     if (const char* df = getenv("LARS_DEFER_FINISH")) h->defer = df[0] == '1';
     const char* kb = getenv("LARS_K1_BULK");
     h->k1_bulk = kb ? kb[0] == '1' : kK1BulkDefault;
-    if (h->k1_bulk &&
-        norms_bulk_blocks_per_sm(hp->grad_dtype, (hp->flags & LARS_FLAG_CARRY_WNORM) != 0) < kCtasPerSm)
-      h->k1_bulk = false;
+    if (h->k1_bulk) {
+      const int occ = norms_bulk_blocks_per_sm(hp->grad_dtype, (hp->flags & LARS_FLAG_CARRY_WNORM) != 0);
+      if (getenv("LARS_VERBOSE")) fprintf(stderr, "[lars] K1 bulk: %d CTAs/SM resident (need %d)\n", occ, kCtasPerSm);
+      if (occ < kCtasPerSm) h->k1_bulk = false;
+    }
   }
   h->full.wl = make_worklist(h->plan, -1, h->sms * kCtasPerSm, min_tile);
   if (device >= 0) {
@@ -706,11 +708,18 @@ lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, cons
     const bool carry = (h->hp.flags & LARS_FLAG_CARRY_WNORM) != 0;
     // F1 through bulk-copy stages (LARS_DP_BULK=0/1 overrides the default) when 4 CTAs per SM stay resident
     const char* db = getenv("LARS_DP_BULK");
-    h->fused.bulk = db ? db[0] == '1' : kDpBulkDefault;
+    // default: bulk-copy F1 for the 8-peer instance (P = 5..8): at P = 4 with LARS_DP_NP=8 it measured
+    // 0.231 ms/step against 0.302 for the register instance (2 CTAs/SM), and 0.223 for the native 4-peer
+    // register instance (profiles/r02_dp4/np8_probe); the 2- and 4-peer instances keep the register loop
+    h->fused.bulk = db ? db[0] == '1' : h->fused.np_template >= 8;
     if (h->fused.bulk &&
         dp_reduce_norms_blocks_per_sm(h->hp.grad_dtype, carry, h->fused.np_template, true) < kCtasPerSm)
       h->fused.bulk = false;
     const int bpsm = dp_reduce_norms_blocks_per_sm(h->hp.grad_dtype, carry, h->fused.np_template, h->fused.bulk);
+    if (getenv("LARS_VERBOSE"))
+      fprintf(stderr, "[lars] rank %d: F1 instance for %d peers, bulk %d (bulk occupancy %d), %d CTAs/SM\n", rank,
+              h->fused.np_template, (int)h->fused.bulk,
+              dp_reduce_norms_blocks_per_sm(h->hp.grad_dtype, carry, h->fused.np_template, true), bpsm);
     if (bpsm <= 0) return LARS_ERR_CUDA;
     h->fused.grid_norm = h->sms * bpsm;
     ntiles_target = h->fused.grid_norm;

@@ -12,10 +12,12 @@ run() {  # name, env..., then torchrun args
     --master-addr=127.0.0.1 --master-port=$((29600 + RANDOM % 300)) tests/dp_worker.py > "$out/$name.log" 2>&1
   echo "dp_worker $name rc=$?" >> "$out/status"
 }
-mkdir -p "$out/cases" "$out/cases_bulk" "$out/cases_np8"
-run cases DP_REPORT_DIR=$out/cases
-run cases_bulk DP_REPORT_DIR=$out/cases_bulk LARS_DP_BULK=1 DP_CASES=^fused
-run cases_np8 DP_REPORT_DIR=$out/cases_np8 LARS_DP_NP=8 DP_CASES=^fused
+if [ "${DP_ROUND_ONLY:-}" != bench ]; then  # DP_ROUND_ONLY=bench: bench lines and traces only
+  mkdir -p "$out/cases" "$out/cases_bulk" "$out/cases_np8"
+  run cases DP_REPORT_DIR=$out/cases
+  run cases_bulk DP_REPORT_DIR=$out/cases_bulk LARS_DP_BULK=1 DP_CASES=^fused
+  run cases_np8 DP_REPORT_DIR=$out/cases_np8 LARS_DP_NP=8 DP_CASES=^fused
+fi
 for v in 0 1; do
   LARS_DP_BULK=$v timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N \
     --master-addr=127.0.0.1 --master-port=$((29900 + v)) bench.py --gpus $N > "$out/bench_bulk$v.json" 2> "$out/bench_bulk$v.err"
