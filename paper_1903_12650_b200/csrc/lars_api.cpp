@@ -708,10 +708,11 @@ lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, cons
     const bool carry = (h->hp.flags & LARS_FLAG_CARRY_WNORM) != 0;
     // F1 through bulk-copy stages (LARS_DP_BULK=0/1 overrides the default) when 4 CTAs per SM stay resident
     const char* db = getenv("LARS_DP_BULK");
-    // default: bulk-copy F1 for the 8-peer instance (P = 5..8): at P = 4 with LARS_DP_NP=8 it measured
-    // 0.231 ms/step against 0.302 for the register instance (2 CTAs/SM), and 0.223 for the native 4-peer
-    // register instance (profiles/r02_dp4/np8_probe); the 2- and 4-peer instances keep the register loop
-    h->fused.bulk = db ? db[0] == '1' : h->fused.np_template >= 8;
+    // default: bulk-copy F1 for the 2- and 8-peer instances. 8 peers (P = 5..8), emulated at P = 4 with
+    // LARS_DP_NP=8: 0.231 ms/step against 0.302 for the register instance at 2 CTAs/SM
+    // (profiles/r02_dp4/np8_probe); P = 2: 0.162 vs 0.166 ms (F1 4-7 us shorter, profiles/r02_dp2). The
+    // 4-peer instance keeps the register loop (0.221 vs 0.227 ms, profiles/r02_dp4).
+    h->fused.bulk = db ? db[0] == '1' : h->fused.np_template != 4;
     if (h->fused.bulk &&
         dp_reduce_norms_blocks_per_sm(h->hp.grad_dtype, carry, h->fused.np_template, true) < kCtasPerSm)
       h->fused.bulk = false;
