@@ -194,7 +194,14 @@ def run_ours(args):
                                grad_scale=1.0 / (G.GRAD_PRESCALE * P), flags=flags, buckets=args.buckets, **HP)
     h = mk(PK.lars.FLAG_CARRY_WNORM if carry else 0)
     if P > 1:
-        h.comm_init_torch()
+        try:
+            h.comm_init_torch()
+        except PK.LarsError as e:  # fused-path setup failed (every rank alike): rerun on the NCCL path
+            print(f"[bench] lars_comm_init failed ({e}); retrying with LARS_DP_FUSED=0", file=sys.stderr)
+            h.close()
+            os.environ["LARS_DP_FUSED"] = "0"
+            h = mk(PK.lars.FLAG_CARRY_WNORM if carry else 0)
+            h.comm_init_torch()
     gbytes = 4 if dtype == "f32" else 2
 
     def dev_flat(arrs):

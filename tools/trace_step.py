@@ -54,6 +54,8 @@ def main():
     if (tr[5, :n2, 0] > 0).all():
         print(f"K2 deferred-finish prologue: min/p50/max = {pro.min():.2f}/{np.median(pro):.2f}/{pro.max():.2f} us")
         for k, what in ((1, "segment records + flags in"), (2, "whole layers finished")):
+            if not (tr[5, :n2, k] > 0).all():
+                continue
             x = (tr[5, :n2, k] - tr[1, :n2, 0]) / 1e3
             print(f"  {what}: min/p50/max = {x.min():.2f}/{np.median(x):.2f}/{x.max():.2f} us")
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
