@@ -22,3 +22,8 @@ timeout 600 python tools/schedule_replay.py > gpurun_out/r152_replay_${TAG}.json
 echo "schedule_replay rc=$?"
 timeout 900 python tools/skew_sweep.py > gpurun_out/skew_sweep_${TAG}.jsonl 2> gpurun_out/skew_sweep_${TAG}.err
 echo "skew_sweep rc=$?"
+# the fused data-parallel kernels F1/F2 through a one-rank communicator (ncu cannot replay a multi-rank run)
+python tools/profile_dp1.py > gpurun_out/plain_dp1_${TAG}.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:lars_dp_ -s 6 -c 2 -o gpurun_out/prof_${TAG}_dp1 \
+    python tools/profile_dp1.py > gpurun_out/ncu_dp1_${TAG}.log 2>&1
+echo "ncu dp1 rc=$?"
