@@ -78,7 +78,7 @@ def _worker(rank, world, port, errors, policy="contiguous"):
         other = PK.Lars([(t.numel, t.kind) for t in (lay if rank == 0 else lay[:-1])], device=-1, nranks=world, **kw)
         hs = [None] * world
         dist.all_gather_object(hs, other.layout_hash())
-        assert hs[0] != hs[1]
+        assert hs[0] != hs[1] and len(set(hs[1:])) == 1
         dist.destroy_process_group()
     except Exception as ex:  # pragma: no cover - surfaced by the parent
         import traceback
@@ -86,14 +86,14 @@ def _worker(rank, world, port, errors, policy="contiguous"):
         errors.put(f"rank {rank}: {ex}\n{traceback.format_exc()}")
 
 
-@pytest.mark.parametrize("policy", ["contiguous", "groups"])
-def test_dp_plan_and_sharded_update_world2_gloo(policy):
+@pytest.mark.parametrize("policy,world", [("contiguous", 2), ("groups", 2), ("contiguous", 4)])
+def test_dp_plan_and_sharded_update_gloo(policy, world):
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     errors = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, errors, policy)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, errors, policy)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
