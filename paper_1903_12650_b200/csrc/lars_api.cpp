@@ -188,6 +188,10 @@ struct lars_ctx {
     bool ok = false;
     void *w = nullptr, *g = nullptr, *x = nullptr;
     ncclWindow_t wwin = nullptr, gwin = nullptr, xwin = nullptr;
+    // second symmetric gradient buffer: dp_allreduce_lars_step_host_grad alternates g / g2 so the copy of
+    // step t+1's gradient overlaps step t (peers read the buffer of the step they are in)
+    void* g2 = nullptr;
+    ncclWindow_t gwin2 = nullptr;
     ncclDevComm dc{};
     bool dc_ok = false;
     float* gred32 = nullptr;
@@ -301,6 +305,9 @@ static lars_status_t setup_fused(lars_ctx* h) {
   CUDA_OR(cudaMemset(f.x, 0, xb));
   NCCL_OR(ncclCommWindowRegister(h->comm, f.w, wb, &f.wwin, NCCL_WIN_COLL_SYMMETRIC));
   NCCL_OR(ncclCommWindowRegister(h->comm, f.g, gb, &f.gwin, NCCL_WIN_COLL_SYMMETRIC));
+  NCCL_OR(ncclMemAlloc(&f.g2, gb));
+  CUDA_OR(cudaMemset(f.g2, 0, gb));
+  NCCL_OR(ncclCommWindowRegister(h->comm, f.g2, gb, &f.gwin2, NCCL_WIN_COLL_SYMMETRIC));
   NCCL_OR(ncclCommWindowRegister(h->comm, f.x, xb, &f.xwin, NCCL_WIN_COLL_SYMMETRIC));
   // one resident wave each (one tile per CTA). F1 is a cooperative launch sized by the occupancy of the
   // exact instance launched (lars_comm_init computed it); launch_dp_fused caps it at one CTA per tile.
@@ -625,6 +632,22 @@ lars_status_t lars_step_dev_iter(lars_handle_t h, float* w, const void* g, float
 static lars_status_t stage_host_grad(lars_handle_t h, const void* g_host, cudaStream_t s);
 static lars_status_t readback_status(lars_handle_t h, const DevBufs& b, cudaStream_t s);
 
+// The copy stream, the per-buffer events and the pinned status mirror of the host-gradient entry points.
+static lars_status_t host_stage_events(lars_handle_t h, cudaStream_t s) {
+  if (h->hcs) return LARS_OK;
+  for (int b = 0; b < 2; ++b) {
+    CUDA_OR(cudaEventCreateWithFlags(&h->hcopied[b], cudaEventDisableTiming));
+    CUDA_OR(cudaEventCreateWithFlags(&h->hconsumed[b], cudaEventDisableTiming));
+    CUDA_OR(cudaEventRecord(h->hconsumed[b], s));
+  }
+  if (!h->pinned && cudaMallocHost(&h->pinned, 256 + 2 * (size_t)h->plan.L * sizeof(double)) != cudaSuccess) {
+    h->pinned = nullptr;
+    return LARS_ERR_OOM;
+  }
+  CUDA_OR(cudaStreamCreateWithFlags(&h->hcs, cudaStreamNonBlocking));
+  return LARS_OK;
+}
+
 lars_status_t lars_step_host_grad(lars_handle_t h, float* w, const void* g_host, float* m, int64_t iter,
                                   void* stream) {
   if (!h || !g_host) return LARS_ERR_INVALID_ARG;
@@ -634,19 +657,13 @@ lars_status_t lars_step_host_grad(lars_handle_t h, float* w, const void* g_host,
   lars_status_t st = check_step_args(h, w, w, m, iter);  // (g is staged: validated below)
   if (st != LARS_OK) return st;
   const size_t gbytes = (size_t)h->plan.padded * dtype_size(h->hp.grad_dtype);
-  if (!h->hcs) {
-    for (int b = 0; b < 2; ++b) {
-      if (cudaMalloc(&h->hstage[b], gbytes) != cudaSuccess) { h->hstage[b] = nullptr; return LARS_ERR_OOM; }
-      CUDA_OR(cudaEventCreateWithFlags(&h->hcopied[b], cudaEventDisableTiming));
-      CUDA_OR(cudaEventCreateWithFlags(&h->hconsumed[b], cudaEventDisableTiming));
-      CUDA_OR(cudaEventRecord(h->hconsumed[b], s));
-    }
-    if (!h->pinned && cudaMallocHost(&h->pinned, 256 + 2 * (size_t)h->plan.L * sizeof(double)) != cudaSuccess) {
-      h->pinned = nullptr;
+  st = host_stage_events(h, s);
+  if (st != LARS_OK) return st;
+  for (int b = 0; b < 2; ++b)
+    if (!h->hstage[b] && cudaMalloc(&h->hstage[b], gbytes) != cudaSuccess) {
+      h->hstage[b] = nullptr;
       return LARS_ERR_OOM;
     }
-    CUDA_OR(cudaStreamCreateWithFlags(&h->hcs, cudaStreamNonBlocking));
-  }
   const int b = h->hnext;
   h->hnext ^= 1;
   // the copy waits only for the step that last read this buffer (two steps ago), not for step t-1
@@ -946,10 +963,10 @@ lars_status_t lars_group_trace_read(lars_handle_t h, void* ref_event, double* re
 
 // Device-side view of the fused path's state for one launch. The 64-byte state block holds, in order: the
 // step epoch, the step's iteration, F1's entry "go" flag and F2's exit counter.
-static DpFused fused_view(lars_handle_t h, int64_t begin) {
+static DpFused fused_view(lars_handle_t h, int64_t begin, ncclWindow_t gwin) {
   DpFused f{};
   f.dc = h->fused.dc;
-  f.gwin = h->fused.gwin;
+  f.gwin = gwin;
   f.wwin = h->fused.wwin;
   f.xwin = h->fused.xwin;
   f.rank = h->rank;
@@ -980,8 +997,8 @@ static lars_status_t dp_impl(lars_handle_t h, float* w, const void* g, float* m,
   hy_half.w_half = h->whalf;  // nullptr unless LARS_FLAG_HALF_WEIGHTS
   const Hyper& hy2 = hy_half;
   auto* pe = h->prof.begin(2);
-  if (h->fused.ok && (void*)w == h->fused.w && g == h->fused.g) {  // fused NVLink path (F1, F2)
-    const DpFused f = fused_view(h, begin);
+  if (h->fused.ok && (void*)w == h->fused.w && (g == h->fused.g || g == h->fused.g2)) {  // fused NVLink path
+    const DpFused f = fused_view(h, begin, g == h->fused.g ? h->fused.gwin : h->fused.gwin2);
     prof_rec(pe, 0, s);
     prof_rec(pe, 1, s);
     CUDA_OR(launch_dp_fused(dt, h->shard.dw, h->shard.sc, hy2, w, m, f, h->fused.grid_norm, h->fused.grid_update, s,
@@ -1070,14 +1087,24 @@ lars_status_t dp_allreduce_lars_step_host_grad(lars_handle_t h, float* w, const 
   cudaStream_t s = (cudaStream_t)stream;
   lars_status_t st;
   const void* gdev;
-  if (h->fused.ok && (void*)w == h->fused.w) {  // fused path: the gradient lands in the symmetric buffer
+  if (h->fused.ok && (void*)w == h->fused.w) {
+    // fused path: the gradient lands in one of the two symmetric buffers, copied on the library's copy stream
+    // so the copy of the next step's gradient overlaps this step (the buffer is reused two steps later, after
+    // this rank's step that read it — and with it every peer's F1, ordered by F2's exit barrier — completed)
     const size_t gbytes = (size_t)h->plan.padded * dtype_size(h->hp.grad_dtype);
-    if (!h->pinned && cudaMallocHost(&h->pinned, 256 + 2 * (size_t)h->plan.L * sizeof(double)) != cudaSuccess) {
-      h->pinned = nullptr;
-      return LARS_ERR_OOM;
-    }
-    CUDA_OR(cudaMemcpyAsync(h->fused.g, g_host, gbytes, cudaMemcpyHostToDevice, s));
-    gdev = h->fused.g;
+    st = host_stage_events(h, s);
+    if (st != LARS_OK) return st;
+    const int b = h->hnext;
+    h->hnext ^= 1;
+    void* gb = b == 0 ? h->fused.g : h->fused.g2;
+    CUDA_OR(cudaStreamWaitEvent(h->hcs, h->hconsumed[b], 0));
+    CUDA_OR(cudaMemcpyAsync(gb, g_host, gbytes, cudaMemcpyHostToDevice, h->hcs));
+    CUDA_OR(cudaEventRecord(h->hcopied[b], h->hcs));
+    CUDA_OR(cudaStreamWaitEvent(s, h->hcopied[b], 0));
+    st = dp_allreduce_lars_step(h, w, gb, m, iter, stream);
+    if (st != LARS_OK) return st;
+    CUDA_OR(cudaEventRecord(h->hconsumed[b], s));
+    return readback_status(h, h->shard, s);
   } else {
     st = stage_host_grad(h, g_host, s);
     if (st != LARS_OK) return st;
@@ -1207,12 +1234,14 @@ lars_status_t lars_destroy(lars_handle_t h) {
       if (f.dc_ok) ncclDevCommDestroy(h->comm, &f.dc);
       if (f.wwin) ncclCommWindowDeregister(h->comm, f.wwin);
       if (f.gwin) ncclCommWindowDeregister(h->comm, f.gwin);
+      if (f.gwin2) ncclCommWindowDeregister(h->comm, f.gwin2);
       if (f.xwin) ncclCommWindowDeregister(h->comm, f.xwin);
       if (h->hwin) ncclCommWindowDeregister(h->comm, h->hwin);
       if (h->whalf && h->whalf_nccl_mem) ncclMemFree(h->whalf);
       if (h->whalf && !h->whalf_nccl_mem) cudaFree(h->whalf);
       if (f.w) ncclMemFree(f.w);
       if (f.g) ncclMemFree(f.g);
+      if (f.g2) ncclMemFree(f.g2);
       if (f.x) ncclMemFree(f.x);
       cudaFree(f.gred32);
       cudaFree(f.state);

@@ -339,6 +339,48 @@ def main():
             print(json.dumps(report), flush=True)
             dist.destroy_process_group()
             sys.exit(1)
+    # host-gradient entry point (dp_allreduce_lars_step_host_grad): five consecutive steps issued without
+    # synchronizing — the fused path alternates its two symmetric gradient buffers, the copy of step k+1
+    # overlapping step k — must equal, bit for bit, the same steps on device gradients; one step's gradient
+    # has a NaN on one rank and is skipped everywhere
+    for fused_h in (True, False):
+        if sel and not re.search(sel, "host-grad-fused" if fused_h else "host-grad-nccl"):
+            continue
+        lay_h = LY.resnet50()[:40]
+        kw_h = hp_kwargs(grad_dtype="f16", grad_scale=1.0 / (G.GRAD_PRESCALE * P), flags=1)
+        hs = [PK.Lars([(x.numel, x.kind) for x in lay_h], device=local, nranks=P, **kw_h) for _ in range(2)]
+        for hh in hs:
+            hh.comm_init_torch()
+        pk = lambda hh, a: torch.from_numpy(G.pack(a, hh.offsets, hh.padded_numel).view(a[0].dtype)).to(dev)
+        grads = [G.grads(lay_h, rank, 30 + k, "f16") for k in range(5)]
+        if rank == (1 % P):
+            grads[2][3] = grads[2][3].copy()
+            grads[2][3][0] = np.nan
+        ws, ms = [], []
+        for hh in hs:
+            w0, m0 = pk(hh, G.weights(lay_h)), pk(hh, G.momentum(lay_h, 1e-3))
+            if fused_h:
+                wsym, _ = hh.dp_buffers()
+                wsym.copy_(w0)
+                w0 = wsym
+            ws.append(w0)
+            ms.append(m0)
+        hosts = [torch.from_numpy(G.pack(gk, hs[0].offsets, hs[0].padded_numel)).pin_memory() for gk in grads]
+        for k in range(5):
+            hs[0].dp_allreduce_lars_step_host_grad(ws[0], hosts[k], ms[0], 700 + k)
+        torch.cuda.synchronize()
+        g_dev = hs[1].dp_buffers()[1] if fused_h else torch.empty_like(hosts[0], device=dev)
+        for k in range(5):
+            g_dev.copy_(hosts[k])
+            hs[1].dp_allreduce_lars_step(ws[1], g_dev, ms[1], 700 + k)
+            torch.cuda.synchronize()
+            assert (hs[1].last_step_status() == 1) == (k == 2), (k, hs[1].last_step_status())
+        same_h = torch.equal(ws[0], ws[1]) and torch.equal(ms[0], ms[1])
+        report["cases"].append({"name": "host-grad-fused" if fused_h else "host-grad-nccl", "bitwise": same_h})
+        if not same_h:
+            report["failures"].append(f"host-grad ({'fused' if fused_h else 'nccl'}) differs from device path")
+        for hh in hs:
+            hh.close()
     # parallel deterministic initialization: every rank initializes its own replica from
     # the same seed; the replicas are bitwise identical with zero bytes broadcast
     lay_i = LY.resnet50()
