@@ -289,7 +289,11 @@ lars_status_t dp_allreduce_lars_step_dev_iter(lars_handle_t h, float* w, const v
 
 /* Same as dp_allreduce_lars_step with the rank's local gradient in HOST memory g_host (pinned for async
  * copies, padded_numel elements): H2D copy into a library staging buffer, the dp step, then a D2H copy of
- * the step status + per-layer norms into library-owned pinned memory, all on `stream`. */
+ * the step status + per-layer norms into library-owned pinned memory. With w = the lars_dp_buffers weight
+ * buffer (fused path) the gradient goes into one of TWO symmetric gradient buffers, alternating per call and
+ * copied on the library's copy stream (ordered before the step on `stream` by an event), so the next call's
+ * copy overlaps this step; every rank must make the same sequence of calls. Otherwise the copy runs on
+ * `stream`. g_host must stay unmodified until the step has completed on `stream`. */
 lars_status_t dp_allreduce_lars_step_host_grad(lars_handle_t h, float* w, const void* g_host, float* m,
                                                int64_t iter, void* stream);
 
