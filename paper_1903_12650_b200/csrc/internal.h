@@ -178,8 +178,6 @@ struct Hyper {
   bool carry;                // LARS_FLAG_CARRY_WNORM
   bool lr_at_apply;          // LARS_FLAG_LR_AT_APPLY (SPEC.md:186 momentum form)
   void* w_half = nullptr;    // LARS_FLAG_HALF_WEIGHTS: compute weights (grad dtype) the update also writes
-  int32_t k2_prefetch = 0;   // K2: chunks per CTA whose w, m are prefetched into L2 before its PDL wait
-  bool k2_prefetch_g = false;  // ... and their gradient
   bool k1_bulk = false;      // K1 streams its chunks through the bulk-copy engine (stream_tile_bulk)
   bool defer = false;        // single GPU: the layer finish moves from K1's tail into K2's prologue
   double lr_host = 0.0;      // lr(iter) from the host's table (host-given iteration; saves K2 a load)

@@ -121,10 +121,6 @@ __device__ __forceinline__ uint4 ld16_keep(const void* p) {
       : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
-// L2 prefetch of a contiguous range by the bulk-copy engine (no registers held; 16 B aligned, 16 B multiple)
-__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 
 // Gradient access by wire dtype. Widening fp16/bf16 -> fp32 is exact.
 template <int DT> struct Grad;
@@ -1069,30 +1065,6 @@ __device__ __forceinline__ void update_item(int32_t item, const DevWork& wk, con
     update_chunk<DT, CARRY, WS, DEFER>(c, wk, sc, hy, w, g, g_shift, m, ws, base);
 }
 
-// Before K2's griddepcontrol.wait (its CTAs become resident as K1's retire): the bulk-copy engine
-// prefetches into L2 the w and m (and optionally g) of the first hy.k2_prefetch chunks this CTA will
-// update — the last chunks of its tile's last part (update_item's order) — so the HBM that K1's
-// layer-finishing tail leaves idle already streams K2's first bytes. Safe: K1 triggered this launch only
-// after its own wait, i.e. after the previous step's K2 completed.
-template <int DT>
-__device__ __forceinline__ void k2_prefetch_first(const DevWork& wk, const Hyper& hy, const float* w, const void* g,
-                                                  int64_t g_shift, const float* m) {
-  const int32_t tile = blockIdx.x;
-  if (tile >= wk.ntiles) return;
-  const int32_t t0 = wk.tile_chunk[tile], tn = wk.tile_chunk[tile + 1] - t0;
-  const int32_t c0 = t0 + (int32_t)((int64_t)tn * (kUpdateSplit - 1) / kUpdateSplit), c1 = t0 + tn;
-  constexpr int kEs = DT == LARS_F32 ? 4 : 2;
-  for (int32_t i = threadIdx.x; i < hy.k2_prefetch && c1 - 1 - i >= c0; i += blockDim.x) {
-    const Seg ck = wk.chunks[c1 - 1 - i];
-    const uint32_t wb = ((uint32_t)ck.len * 4u) & ~15u, gb = ((uint32_t)ck.len * kEs) & ~15u;
-    if (wb) {
-      prefetch_l2_bulk(w + ck.begin, wb);
-      prefetch_l2_bulk(m + ck.begin, wb);
-    }
-    if (hy.k2_prefetch_g && gb) prefetch_l2_bulk((const char*)g + (ck.begin - g_shift) * kEs, gb);
-  }
-}
-
 // Deferred finish (single GPU, hy.defer). K1 has left every segment's partial sums, one non-finite flag
 // per K1 CTA and (device iteration) the step's iteration. Before griddepcontrol.wait (while K1 drains) a
 // K2 CTA copies its tile's segment records (static work list) into shared memory; after the wait it reads
@@ -1211,8 +1183,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_update_kernel(DevWo
                                                                            int64_t g_shift, float* __restrict__ m) {
   static_assert(!(HALF && DEFER), "the deferred finish is the whole-layout step's");
   pdl_trigger();
-  // K1 writes none of w, g, m: while K1 drains, pull the first chunks this CTA updates into L2
-  if (hy.k2_prefetch > 0) k2_prefetch_first<DT>(wk, hy, w, g, g_shift, m);
   if constexpr (DEFER) deferred_prefetch_segs(blockIdx.x, wk);  // static work list: before the wait
   pdl_wait();
   bool skip = false;

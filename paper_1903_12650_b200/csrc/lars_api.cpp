@@ -203,8 +203,6 @@ struct lars_ctx {
   } fused;
   bool k1_bulk = false;     // Hyper::k1_bulk (LARS_K1_BULK)
   bool defer = kDeferDefault;  // Hyper::defer for lars_step (LARS_DEFER_FINISH)
-  int32_t k2_prefetch = 0;  // Hyper::k2_prefetch (LARS_K2_PREFETCH)
-  bool k2_prefetch_g = false;
   int32_t last_red_dtype = LARS_F16;
   const void* last_red = nullptr;
   // bucketed NCCL schedule (hp.buckets = K >= 2): bucket k of rank r covers shard-relative elements
@@ -390,11 +388,6 @@ lars_status_t lars_init(const lars_tensor_t* tensors, int32_t n, const lars_hpar
   if (st != LARS_OK) { delete h; return st; }
   h->hp = *hp;
   h->device = device;
-  // K2's L2 prefetch of its first chunks while K1 drains (chunks per CTA; "g" suffix: gradient too)
-  if (const char* pf = getenv("LARS_K2_PREFETCH")) {
-    h->k2_prefetch = std::max(0, atoi(pf));
-    h->k2_prefetch_g = std::strchr(pf, 'g') != nullptr;
-  }
   const int32_t min_tile = hp->tile_elems > 0 ? hp->tile_elems : kDefaultMinTile;
   if (device >= 0) {
     DeviceGuard g(device);
@@ -580,10 +573,8 @@ static Hyper hyper(lars_handle_t h, int64_t iter, int64_t* iter_dev = nullptr) {
   Hyper hy{h->lr_d, iter, iter_dev, h->plan.T, h->hp.eta, h->hp.weight_decay, h->hp.eps, h->hp.grad_scale,
            (float)h->hp.momentum, (float)h->hp.grad_scale, (h->hp.flags & LARS_FLAG_CARRY_WNORM) != 0,
            (h->hp.flags & LARS_FLAG_LR_AT_APPLY) != 0};
-  hy.k2_prefetch = h->k2_prefetch;
   hy.k1_bulk = h->k1_bulk;
   if (!iter_dev && iter >= 0 && iter < (int64_t)h->plan.lr.size()) hy.lr_host = h->plan.lr[iter];
-  hy.k2_prefetch_g = h->k2_prefetch_g;
   return hy;
 }
 

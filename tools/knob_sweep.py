@@ -1,7 +1,7 @@
 #!/usr/bin/env python
-"""Single-GPU lars_step timing over environment knobs read at lars_init (e.g. LARS_K2_PREFETCH).
+"""Single-GPU lars_step timing over environment knobs read at lars_init (e.g. LARS_DEFER_FINISH).
 
-    python tools/knob_sweep.py --knob LARS_K2_PREFETCH --values 0,8,16,32,16g --dtype f32,f16
+    python tools/knob_sweep.py --knob LARS_DEFER_FINISH --values 0,1 --dtype f32,f16
 
 Each (dtype, value) gets a fresh handle on the same device buffers (ResNet-50 layout by default, carried
 weight norms as in bench.py); the step is timed with CUDA events over --steps steps, --reps times,
@@ -21,8 +21,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--knob", default="LARS_K2_PREFETCH")
-    ap.add_argument("--values", default="0,8,16,32")
+    ap.add_argument("--knob", default="LARS_DEFER_FINISH")
+    ap.add_argument("--values", default="0,1")
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--layout", default="resnet50")
     ap.add_argument("--steps", type=int, default=200)
