@@ -42,3 +42,14 @@ n = NvlinkCounters(0)
 print(n.describe())
 n.start(); time.sleep(0.2); print(n.stop())
 PY
+# configs[3] and configs[4] at P = N (fused NVLink path; --nccl for the NCCL path)
+if [ "${DP_ROUND_EXTRA:-0}" = 1 ]; then
+  for extra in "" "--nccl"; do
+    timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr=127.0.0.1 \
+      --master-port=29960 tools/schedule_replay.py $extra >> "$out/r152_replay.jsonl" 2>> "$out/r152_replay.err"
+    echo "schedule_replay $extra rc=$?" >> "$out/status"
+  done
+  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr=127.0.0.1 \
+    --master-port=29961 tools/skew_dp.py > "$out/skew_dp_1b.jsonl" 2> "$out/skew_dp_1b.err"
+  echo "skew_dp rc=$?" >> "$out/status"
+fi

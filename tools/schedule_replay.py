@@ -114,7 +114,10 @@ def main():
         if a.out:
             with open(a.out, "a") as f:
                 f.write(json.dumps(res) + "\n")
-    del graphs
+    for gr in graphs:  # release every graph (NCCL work captured in them) before the communicator goes
+        gr.reset()
+    torch.cuda.synchronize()
+    del graphs, gr
     h.close()
     if dist:
         dist.destroy_process_group()
