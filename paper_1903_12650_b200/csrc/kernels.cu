@@ -1014,7 +1014,13 @@ __device__ __forceinline__ void update_chunk(int32_t c, const DevWork& wk, const
     if (CARRY) aw = fma((double)wn, (double)wn, aw);
   }
   int32_t j = ng - 1 - lane;
-  for (; j - 32 >= 0; j -= 64) {
+// One 8-element group (w, g, m: 3 x 32 B loads) per lane per iteration: the two-group unroll of round 1
+// needed > 64 registers and spilled inside this loop; one group is spill-free (59 registers) and measured
+// 3.0-3.5 us per step faster (profiles/r02_k2_pairs_sweep.txt). LARS_K2_PAIRS=1 restores the pairs.
+#ifndef LARS_K2_PAIRS
+#define LARS_K2_PAIRS 0
+#endif
+  for (; LARS_K2_PAIRS && j - 32 >= 0; j -= 64) {
     const int32_t j1 = j - 32;
     F8 w0 = ld8_rw(wp + 8 * j), w1 = ld8_rw(wp + 8 * j1);
     const F8 g0 = Grad<DT>::load8(g, gi + 8 * j), g1 = Grad<DT>::load8(g, gi + 8 * j1);
@@ -1032,7 +1038,7 @@ __device__ __forceinline__ void update_chunk(int32_t c, const DevWork& wk, const
       accw8(aw, w1);
     }
   }
-  if (j >= 0) {
+  for (; j >= 0; j -= 32) {  // (LARS_K2_PAIRS = 0: one 8-element group per lane per iteration throughout)
     F8 w0 = ld8_rw(wp + 8 * j), m0 = ld8_rw(mp + 8 * j);
     const F8 g0 = Grad<DT>::load8(g, gi + 8 * j);
     upd8(w0, m0, g0, s, cf, b, mu, hy.lr_at_apply);
