@@ -988,7 +988,9 @@ __shared__ __align__(16) SegInfo k2_seg[kMaxTileChunks];
 
 // DEFER: lr*lambda and beta_l come from the CTA's shared copies (k2_coef/k2_beta, index tensor - base),
 // otherwise from the scratch arrays K1 (or the split finisher) wrote.
-template <int DT, bool CARRY, typename WS = NoPeers, bool DEFER = false>
+// PAIRS: two 8-element groups per lane per iteration (more stores in flight: the fused F2, whose peer stores
+// bound it, measured 1.8 us faster at P = 2) or one (K2: spill-free at 59 registers, 3.0-3.5 us faster).
+template <int DT, bool CARRY, typename WS = NoPeers, bool DEFER = false, bool PAIRS = false>
 __device__ __forceinline__ void update_chunk(int32_t c, const DevWork& wk, const DevScratch& sc, const Hyper& hy,
                                              float* __restrict__ w, const void* __restrict__ g, int64_t g_shift,
                                              float* __restrict__ m, const WS& ws, int32_t base) {
@@ -1014,13 +1016,7 @@ __device__ __forceinline__ void update_chunk(int32_t c, const DevWork& wk, const
     if (CARRY) aw = fma((double)wn, (double)wn, aw);
   }
   int32_t j = ng - 1 - lane;
-// One 8-element group (w, g, m: 3 x 32 B loads) per lane per iteration: the two-group unroll of round 1
-// needed > 64 registers and spilled inside this loop; one group is spill-free (59 registers) and measured
-// 3.0-3.5 us per step faster (profiles/r02_k2_pairs_sweep.txt). LARS_K2_PAIRS=1 restores the pairs.
-#ifndef LARS_K2_PAIRS
-#define LARS_K2_PAIRS 0
-#endif
-  for (; LARS_K2_PAIRS && j - 32 >= 0; j -= 64) {
+  for (; PAIRS && j - 32 >= 0; j -= 64) {
     const int32_t j1 = j - 32;
     F8 w0 = ld8_rw(wp + 8 * j), w1 = ld8_rw(wp + 8 * j1);
     const F8 g0 = Grad<DT>::load8(g, gi + 8 * j), g1 = Grad<DT>::load8(g, gi + 8 * j1);
@@ -1038,7 +1034,7 @@ __device__ __forceinline__ void update_chunk(int32_t c, const DevWork& wk, const
       accw8(aw, w1);
     }
   }
-  for (; j >= 0; j -= 32) {  // (LARS_K2_PAIRS = 0: one 8-element group per lane per iteration throughout)
+  for (; j >= 0; j -= 32) {  // (!PAIRS: one 8-element group per lane per iteration throughout)
     F8 w0 = ld8_rw(wp + 8 * j), m0 = ld8_rw(mp + 8 * j);
     const F8 g0 = Grad<DT>::load8(g, gi + 8 * j);
     upd8(w0, m0, g0, s, cf, b, mu, hy.lr_at_apply);
@@ -1054,7 +1050,7 @@ __device__ __forceinline__ void update_chunk(int32_t c, const DevWork& wk, const
   }
 }
 
-template <int DT, bool CARRY, typename WS = NoPeers, bool DEFER = false>
+template <int DT, bool CARRY, typename WS = NoPeers, bool DEFER = false, bool PAIRS = false>
 __device__ __forceinline__ void update_item(int32_t item, const DevWork& wk, const DevScratch& sc, const Hyper& hy,
                                             float* __restrict__ w, const void* __restrict__ g, int64_t g_shift,
                                             float* __restrict__ m, const WS& ws = WS(), int32_t base = 0) {
@@ -1068,7 +1064,7 @@ __device__ __forceinline__ void update_item(int32_t item, const DevWork& wk, con
   const int32_t c1 = t0 + (int32_t)((int64_t)tn * (q + 1) / kUpdateSplit);
   LARS_DCHECK(tile >= 0 && tile < wk.ntiles && q >= 0 && q < kUpdateSplit && c0 <= c1 && c1 <= wk.nchunks);
   for (int32_t c = c1 - 1 - warp; c >= c0; c -= kWarps)  // backwards: K1's most recent reads first
-    update_chunk<DT, CARRY, WS, DEFER>(c, wk, sc, hy, w, g, g_shift, m, ws, base);
+    update_chunk<DT, CARRY, WS, DEFER, PAIRS>(c, wk, sc, hy, w, g, g_shift, m, ws, base);
 }
 
 // Deferred finish (single GPU, hy.defer). K1 has left every segment's partial sums, one non-finite flag
@@ -1437,18 +1433,18 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_dp_update_gather_ke
       ws.n = f.nranks;
       for (int p = 0; p < f.nranks; ++p) ws.ph[p] = (uint16_t*)ncclGetLsaPointer(f.hwin, 0, p);
       for (int32_t item = blockIdx.x; item < wk.ntiles * kUpdateSplit; item += gridDim.x)
-        update_item<LARS_F32, CARRY, PeerHalf<HDT>>(item, wk, sc, hy, w, f.gred, f.begin, m, ws);
+        update_item<LARS_F32, CARRY, PeerHalf<HDT>, false, true>(item, wk, sc, hy, w, f.gred, f.begin, m, ws);
     } else if (MCAST) {
       const McastWeights ws{(float*)ncclGetLsaMultimemPointer(f.wwin, 0, f.dc)};
       for (int32_t item = blockIdx.x; item < wk.ntiles * kUpdateSplit; item += gridDim.x)
-        update_item<LARS_F32, CARRY, McastWeights>(item, wk, sc, hy, w, f.gred, f.begin, m, ws);
+        update_item<LARS_F32, CARRY, McastWeights, false, true>(item, wk, sc, hy, w, f.gred, f.begin, m, ws);
     } else {
       PeerWeights ws;
       ws.n = 0;
       for (int p = 0; p < f.nranks; ++p)
         if (p != f.rank) ws.pw[ws.n++] = (float*)ncclGetLsaPointer(f.wwin, 0, p);
       for (int32_t item = blockIdx.x; item < wk.ntiles * kUpdateSplit; item += gridDim.x)
-        update_item<LARS_F32, CARRY, PeerWeights>(item, wk, sc, hy, w, f.gred, f.begin, m, ws);
+        update_item<LARS_F32, CARRY, PeerWeights, false, true>(item, wk, sc, hy, w, f.gred, f.begin, m, ws);
     }
   }
   if (MCAST) asm volatile("fence.acq_rel.sys;" ::: "memory");  // multicast stores before the barrier release
