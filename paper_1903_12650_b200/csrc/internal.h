@@ -38,7 +38,10 @@ constexpr int kCtasPerSm = LARS_NORM_CTAS_PER_SM;      // K1 resident CTAs per S
 #endif
 constexpr int dp_norm_ctas_per_sm(int nranks) { return nranks <= 2 ? LARS_DP_CTAS2 : 2; }
 constexpr int32_t kMaxTileChunks = 256; // chunk partials of one tile live in shared memory
-constexpr int32_t kUpdateSplit = 4;     // K2 walks each tile in 4 parts, last part first
+#ifndef LARS_UPDATE_SPLIT
+#define LARS_UPDATE_SPLIT 4
+#endif
+constexpr int32_t kUpdateSplit = LARS_UPDATE_SPLIT;  // K2 walks each tile in parts, last part first
 constexpr int kNormUnroll = LARS_NORM_UNROLL;  // K1 vector groups per lane per iteration
 constexpr int32_t kDefaultMinTile = 4096;
 constexpr bool kK1BulkDefault = false;  // K1 bulk-copy streaming (Hyper::k1_bulk) unless LARS_K1_BULK says
