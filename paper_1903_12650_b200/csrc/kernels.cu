@@ -457,8 +457,14 @@ __device__ __forceinline__ bool finish_core(int32_t l, double sw, double sg, con
 // transaction count. The warp sums squares from shared memory in fp64 (fixed order: lane, piece, then the
 // xor butterfly), the < 8 ragged elements at a tensor's end straight from global memory. Gradient and
 // weight bytes are fetched with an L2 evict_last policy (K2 re-reads them).
-constexpr int kBulkStages = 3;                 // per warp
-constexpr int kBulkStageBytes = 2048;
+#ifndef LARS_BULK_STAGES
+#define LARS_BULK_STAGES 3
+#endif
+#ifndef LARS_BULK_STAGE_BYTES
+#define LARS_BULK_STAGE_BYTES 2048
+#endif
+constexpr int kBulkStages = LARS_BULK_STAGES;  // per warp
+constexpr int kBulkStageBytes = LARS_BULK_STAGE_BYTES;
 constexpr int kBulkSmem = kThreads / 32 * kBulkStages * kBulkStageBytes;  // 48 KB dynamic shared memory
 
 // GL: LocalGrad<DT> (K1: one gradient source) or PeerSumGrad<DT, NP> (F1: the gradient of every rank, read

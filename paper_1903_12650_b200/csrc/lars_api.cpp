@@ -721,9 +721,8 @@ lars_status_t lars_comm_init(lars_handle_t h, int32_t nranks, int32_t rank, cons
     // (profiles/r02_dp4/np8_probe); P = 2: 0.162 vs 0.166 ms (F1 4-7 us shorter, profiles/r02_dp2). The
     // 4-peer instance keeps the register loop (0.221 vs 0.227 ms, profiles/r02_dp4).
     h->fused.bulk = db ? db[0] == '1' : h->fused.np_template != 4;
-    if (h->fused.bulk &&
-        dp_reduce_norms_blocks_per_sm(h->hp.grad_dtype, carry, h->fused.np_template, true) < kCtasPerSm)
-      h->fused.bulk = false;
+    if (h->fused.bulk && dp_reduce_norms_blocks_per_sm(h->hp.grad_dtype, carry, h->fused.np_template, true) < 2)
+      h->fused.bulk = false;  // (F1's work list is cut for whatever residency the instance gets)
     const int bpsm = dp_reduce_norms_blocks_per_sm(h->hp.grad_dtype, carry, h->fused.np_template, h->fused.bulk);
     if (getenv("LARS_VERBOSE"))
       fprintf(stderr, "[lars] rank %d: F1 instance for %d peers, bulk %d (bulk occupancy %d), %d CTAs/SM\n", rank,
