@@ -1294,40 +1294,67 @@ __device__ __forceinline__ unsigned long long share_word(uint32_t epoch, uint32_
 // iteration of this step is recorded (and a device iteration advanced) here, after every layer of this rank
 // has read it.
 __device__ void dp_publish_shares(const DevWork& wk, const DevScratch& sc, const Hyper& hy, const DpFused& f) {
+  // one warp: every (rank, value) word pair by its own lane, all loads of the shares in flight at once
+  const int lane = threadIdx.x & 31;
   const int32_t n = 1 + 2 * wk.nsplit_total;
-  const unsigned long long epoch = *f.epoch + 1ull;
-  *f.epoch = epoch;
-  const int64_t t = hy.iter_dev ? *(volatile int64_t*)hy.iter_dev : hy.iter;
-  *f.step_iter = t;
-  if (hy.iter_dev) *(volatile int64_t*)hy.iter_dev = t + 1;
-  const uint32_t e32 = (uint32_t)epoch;
-  for (int p = 0; p < f.nranks; ++p) {
+  unsigned long long epoch = 0;
+  if (lane == 0) {
+    epoch = *f.epoch + 1ull;
+    *f.epoch = epoch;
+    const int64_t t = hy.iter_dev ? *(volatile int64_t*)hy.iter_dev : hy.iter;
+    *f.step_iter = t;
+    if (hy.iter_dev) *(volatile int64_t*)hy.iter_dev = t + 1;
+  }
+  const uint32_t e32 = (uint32_t)__shfl_sync(0xffffffffu, epoch, 0);
+  for (int32_t k = lane; k < f.nranks * n; k += 32) {
+    const int p = k / n, i = k % n;
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(__ldcg(sc.c3 + i));
     unsigned long long* slot =
         (unsigned long long*)ncclGetLsaPointer(f.xwin, (size_t)f.rank * 2 * n * sizeof(unsigned long long), p);
-    for (int32_t i = 0; i < n; ++i) {
-      const unsigned long long bits = (unsigned long long)__double_as_longlong(sc.c3[i]);
-      cuda::atomic_ref<unsigned long long, cuda::thread_scope_system> lo(slot[2 * i]), hi(slot[2 * i + 1]);
-      lo.store(share_word(e32, (uint32_t)bits), cuda::memory_order_relaxed);
-      hi.store(share_word(e32, (uint32_t)(bits >> 32)), cuda::memory_order_relaxed);
-    }
+    cuda::atomic_ref<unsigned long long, cuda::thread_scope_system> lo(slot[2 * i]), hi(slot[2 * i + 1]);
+    lo.store(share_word(e32, (uint32_t)bits), cuda::memory_order_relaxed);
+    hi.store(share_word(e32, (uint32_t)(bits >> 32)), cuda::memory_order_relaxed);
   }
-  for (int32_t i = 0; i < n; ++i) sc.c3[i] = 0.0;  // next step's shares start from zero
+  __syncwarp();  // every lane has read the shares
+  for (int32_t i = lane; i < n; i += 32) sc.c3[i] = 0.0;  // next step's shares start from zero
 }
 
 // Start of F2 (warp 0 of every CTA): wait until every word of every rank's shares carries this step's
 // epoch, sum the shares in rank order (identical on every rank), finish the split layers this rank touches,
 // decide the skip. Returns the step status (0 apply, 1 non-finite, 2 iteration out of range) to every lane
 // of warp 0.
-__device__ int32_t dp_collect_shares(const DevWork& wk, const DevScratch& sc, const Hyper& hy, const DpFused& f) {
+// The split layer lane k of warp 0 finishes (static work list: loaded before F2's griddepcontrol.wait, so the
+// chain split_locals -> tsplit -> tlars is off the critical path).
+struct SplitPre {
+  int32_t l = -1, j = 0, lars = 0;
+};
+__device__ __forceinline__ SplitPre load_split_pre(const DevWork& wk) {
+  SplitPre sp;
+  const int lane = threadIdx.x & 31;
+  LARS_DCHECK(wk.nsplit_local <= 32);
+  if (lane < wk.nsplit_local) {
+    sp.l = wk.split_locals[lane];
+    sp.j = wk.tsplit[sp.l];
+    sp.lars = wk.tlars[sp.l];
+  }
+  return sp;
+}
+
+__device__ int32_t dp_collect_shares(const DevWork& wk, const DevScratch& sc, const Hyper& hy, const DpFused& f,
+                                     const SplitPre& sp) {
   const int lane = threadIdx.x & 31;
   const int32_t n = 1 + 2 * wk.nsplit_total;
   const uint32_t e32 = (uint32_t)*(volatile unsigned long long*)f.epoch;
+  // the step's iteration as recorded by F1 (a device iteration has moved on already); its lr(t) from the host
+  // unless the iteration lives on the device
+  const int64_t t = *(volatile const int64_t*)f.step_iter;
   unsigned long long* x = (unsigned long long*)ncclGetLocalPointer(f.xwin, 0);
   for (int32_t k = lane; k < f.nranks * 2 * n; k += 32) {
     cuda::atomic_ref<unsigned long long, cuda::thread_scope_system> word(x[k]);
     while ((uint32_t)(word.load(cuda::memory_order_relaxed) >> 32) != e32) __nanosleep(32);
   }
   __syncwarp();
+  TRACE_MARK_AT(6, 1)
   auto val = [&](int p, int32_t i) {  // every word of this step is in: plain reads
     const unsigned long long* w = x + ((size_t)p * n + i) * 2;
     const unsigned long long lo = *(volatile const unsigned long long*)w, hi = *(volatile const unsigned long long*)(w + 1);
@@ -1339,21 +1366,18 @@ __device__ int32_t dp_collect_shares(const DevWork& wk, const DevScratch& sc, co
     for (int p = 0; p < f.nranks; ++p) tot += val(p, i);  // rank order
     bad |= (i == 0) ? (tot > 0.0) : !isfinite(tot);
   }
-  Hyper h2 = hy;  // the step's iteration as recorded by F1 (a device iteration has moved on already)
-  h2.iter = *(volatile const int64_t*)f.step_iter;
-  h2.iter_dev = nullptr;
-  for (int32_t k = lane; k < wk.nsplit_local; k += 32) {
-    const int32_t l = wk.split_locals[k], j = wk.tsplit[l];
+  const bool in_range = t >= 0 && t < hy.total_iters;
+  if (sp.l >= 0) {
     double sw = 0.0, sg = 0.0;
     for (int p = 0; p < f.nranks; ++p) {
-      sw += val(p, 1 + 2 * j);
-      sg += val(p, 2 + 2 * j);
+      sw += val(p, 1 + 2 * sp.j);
+      sg += val(p, 2 + 2 * sp.j);
     }
-    bad |= finish_core(l, sw, sg, wk, sc, h2);  // identical values from every CTA (benign duplicate stores)
+    const StepLr slr{!in_range ? 0.0 : hy.iter_dev ? hy.lr_table[t] : hy.lr_host, in_range};
+    bad |= finish_core(sp.l, sp.lars, sw, sg, sc, hy, slr);  // identical values from every CTA (benign duplicates)
   }
   bad = __any_sync(0xffffffffu, bad);
-  const bool out_of_range = h2.iter < 0 || h2.iter >= hy.total_iters;
-  return out_of_range ? 2 : bad ? 1 : 0;
+  return !in_range ? 2 : bad ? 1 : 0;
 }
 
 // BULK: the rank sum streams through bulk-copy stages (stream_tile_bulk; peer reads by the TMA engine, no
@@ -1401,7 +1425,10 @@ __global__ void __launch_bounds__(kThreads, BULK ? kCtasPerSm : dp_norm_ctas_per
   // overhead outweighs the shorter tail (tools/trace_dp.py)
   const bool final_cta = norms_body<CARRY, PeerSumGrad<DT, NP>, !BULK>(wk, sc, hy, w, gl, BULK ? f1_stages : nullptr);
   TRACE_MARK(4)
-  if (final_cta || (wk.ntensors == 0 && blockIdx.x == 0 && threadIdx.x == 0)) dp_publish_shares(wk, sc, hy, f);
+  __shared__ int s_publish;
+  if (threadIdx.x == 0) s_publish = final_cta || (wk.ntensors == 0 && blockIdx.x == 0);
+  __syncthreads();
+  if (s_publish && threadIdx.x < 32) dp_publish_shares(wk, sc, hy, f);
   __syncthreads();
   TRACE_END(2)
 }
@@ -1413,9 +1440,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_dp_update_gather_ke
   __shared__ int32_t s_status;
   TRACE_BEGIN
   pdl_trigger();
+  SplitPre sp;
+  if (threadIdx.x < 32) sp = load_split_pre(wk);
   pdl_wait();  // F1 complete (its shares and reduced shard are visible)
+  TRACE_MARK_AT(6, 0)
   if (threadIdx.x < 32) {
-    const int32_t st = dp_collect_shares(wk, sc, hy, f);
+    const int32_t st = dp_collect_shares(wk, sc, hy, f, sp);
     if (threadIdx.x == 0) {
       s_status = st;
       if (blockIdx.x == 0) *(volatile int32_t*)sc.skip = st;

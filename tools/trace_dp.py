@@ -67,8 +67,11 @@ def main():
     pre = us(tr[4][:n1, 2])
     coll = us(tr[4][:n2, 0])
     last = int(np.argmax(f1e))
+    waited = us(tr[6][:n2, 0])
+    polled = us(tr[6][:n2, 1])
+    print(f"rank {rank}: F2 shares polled in {q(polled)}", flush=True)
     print(f"rank {rank}: final F1 CTA {last}: tile done {pre[last]:.1f} end {f1e[last]:.1f}; "
-          f"F2 shares collected {q(coll)}", flush=True)
+          f"F2 past griddepcontrol.wait {q(waited)}; F2 shares collected {q(coll)}", flush=True)
     print(f"rank {rank}: F1 ctas {n1}: start {q(f1s)}  past-barrier {q(bar)}  end {q(f1e)} | "
           f"F2 ctas {n2}: start {q(f2s)} end(before exit barrier) {q(f2e)}", flush=True)
     dist.destroy_process_group()
