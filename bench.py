@@ -182,6 +182,11 @@ def run_ours(args):
     rank, P = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", args.gpus))
     local = int(os.environ.get("LOCAL_RANK", 0))
     assert P == args.gpus, f"WORLD_SIZE={P} but --gpus {args.gpus}"
+    t_start = time.time()
+
+    def phase(name):  # progress on stderr (locates a stall in a log)
+        print(f"[bench] rank {rank} +{time.time() - t_start:.1f}s {name}", file=sys.stderr, flush=True)
+
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if P > 1:
@@ -202,6 +207,7 @@ def run_ours(args):
             os.environ["LARS_DP_FUSED"] = "0"
             h = mk(PK.lars.FLAG_CARRY_WNORM if carry else 0)
             h.comm_init_torch()
+    phase("handle ready")
     gbytes = 4 if dtype == "f32" else 2
 
     def dev_flat(arrs):
@@ -241,6 +247,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    phase("warm-up")
     run(args.warmup)
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
@@ -260,6 +267,7 @@ def run_ours(args):
             nvl = None
     barrier()
     torch.cuda.synchronize()
+    phase("timed steps")
     if nvl:
         try:
             nvl.start()
@@ -282,6 +290,7 @@ def run_ours(args):
 
     # per-phase device times (library CUDA events on the same stream; separate pass)
     nprof = min(args.steps, 200)
+    phase("phase timing")
     h.profile_enable(True)
     barrier()
     run(nprof)
@@ -306,6 +315,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         return round(max_over_ranks(e4.elapsed_time(e5)) / args.steps, 5)
 
+    phase("alternatives")
     if P == 1 and carry:
         h0 = mk(0)
         alt["no_carry_ms_per_step"] = time_loop(h0.lars_step, w, g)
@@ -359,6 +369,7 @@ def run_ours(args):
         alt["half_weights_path"] = "fused-nvlink" if fused else "nccl"
         hh.close()
 
+    phase("e2e")
     # end to end through the public API with host gradients
     g_pin = torch.from_numpy(G.pack(g_host, h.offsets, h.padded_numel)).pin_memory()  # lands in g's buffer
     step_h = h.lars_step_host_grad if P == 1 else h.dp_allreduce_lars_step_host_grad
@@ -456,6 +467,7 @@ def run_ours(args):
     }
     if P == 1 and rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(lay, w_host, [g_host], m_host, dtype, P)
+    phase("done")
     if rank == 0:
         emit(out)
     if P > 1:

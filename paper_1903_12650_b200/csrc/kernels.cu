@@ -1507,12 +1507,15 @@ static void launch_reduce_norms_np(int np, int grid, cudaStream_t st, const DevW
                                    const Hyper& hy, const float* w, const DpFused& f) {
   // cooperative: every CTA waits for CTA 0's entry flag, so the whole grid must be co-resident
   const size_t smem = BULK ? kBulkSmem : 0;
+#ifndef LARS_F1_COOP
+#define LARS_F1_COOP 1
+#endif
   if (np <= 2)
-    launch_pdl_smem(lars_dp_reduce_norms_kernel<DT, CARRY, 2, BULK>, grid, st, true, smem, wk, sc, hy, w, f);
+    launch_pdl_smem(lars_dp_reduce_norms_kernel<DT, CARRY, 2, BULK>, grid, st, LARS_F1_COOP, smem, wk, sc, hy, w, f);
   else if (np <= 4)
-    launch_pdl_smem(lars_dp_reduce_norms_kernel<DT, CARRY, 4, BULK>, grid, st, true, smem, wk, sc, hy, w, f);
+    launch_pdl_smem(lars_dp_reduce_norms_kernel<DT, CARRY, 4, BULK>, grid, st, LARS_F1_COOP, smem, wk, sc, hy, w, f);
   else
-    launch_pdl_smem(lars_dp_reduce_norms_kernel<DT, CARRY, 8, BULK>, grid, st, true, smem, wk, sc, hy, w, f);
+    launch_pdl_smem(lars_dp_reduce_norms_kernel<DT, CARRY, 8, BULK>, grid, st, LARS_F1_COOP, smem, wk, sc, hy, w, f);
 }
 
 // Bulk-copy instances: static + dynamic shared memory exceeds the 48 KB a kernel gets without opting in,
