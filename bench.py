@@ -471,6 +471,11 @@ def run_ours(args):
     if rank == 0:
         emit(out)
     if P > 1:
+        # every rank releases its communicator and symmetric windows at the same point (not in garbage-
+        # collection order at interpreter exit)
+        torch.cuda.synchronize()
+        dist.barrier()
+        h.close()
         dist.destroy_process_group()
     del np
 
