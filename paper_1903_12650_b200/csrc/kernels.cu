@@ -111,16 +111,6 @@ __device__ __forceinline__ uint4 ld16_nc(const void* p) {
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
-// read-only, keep in L2 for K2 (the .L2::evict_last qualifier takes 256-bit vectors only; a 128-bit load
-// carries the same priority as an L2 cache-hint policy)
-__device__ __forceinline__ uint4 ld16_keep(const void* p) {
-  uint4 r;
-  asm("{\n\t.reg .b64 pol;\n\t"
-      "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
-      "ld.global.nc.L1::no_allocate.L2::cache_hint.v4.b32 {%0,%1,%2,%3}, [%4], pol;\n\t}"
-      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-  return r;
-}
 
 // Gradient access by wire dtype. Widening fp16/bf16 -> fp32 is exact.
 template <int DT> struct Grad;
@@ -157,14 +147,17 @@ __device__ __forceinline__ F8 widen_b8(uint4 r) {
   return o;
 }
 template <> struct Grad<LARS_F16> {
-  __device__ __forceinline__ static F8 load8_keep(const void* g, int64_t i) { return widen_h8(ld16_keep((const __half*)g + i)); }
+// 16-bit gradients carry NO L2 keep hint in K1: the .L2::evict_last qualifier exists for 256-bit loads
+// only, and a 128-bit load with an evict_last cache-hint policy measured 13.7 us (fp16) / 6.8 us (bf16)
+// slower per step than a plain load (profiles/r02_h16_keep_sweep.txt).
+  __device__ __forceinline__ static F8 load8_keep(const void* g, int64_t i) { return widen_h8(ld16_nc((const __half*)g + i)); }
   __device__ __forceinline__ static F8 load8(const void* g, int64_t i) { return widen_h8(ld16_nc((const __half*)g + i)); }
   __device__ __forceinline__ static float load1(const void* g, int64_t i) { return __half2float(((const __half*)g)[i]); }
   __device__ __forceinline__ static uint4 raw8(const void* g, int64_t i) { return ld16_nc((const __half*)g + i); }
   __device__ __forceinline__ static F8 widen(const uint4& r) { return widen_h8(r); }
 };
 template <> struct Grad<LARS_BF16> {
-  __device__ __forceinline__ static F8 load8_keep(const void* g, int64_t i) { return widen_b8(ld16_keep((const uint16_t*)g + i)); }
+  __device__ __forceinline__ static F8 load8_keep(const void* g, int64_t i) { return widen_b8(ld16_nc((const uint16_t*)g + i)); }
   __device__ __forceinline__ static F8 load8(const void* g, int64_t i) { return widen_b8(ld16_nc((const uint16_t*)g + i)); }
   __device__ __forceinline__ static float load1(const void* g, int64_t i) {
     return __uint_as_float((uint32_t)((const uint16_t*)g)[i] << 16);
@@ -654,12 +647,13 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
     double aw = 0.0, ag = 0.0, aw1 = 0.0, ag1 = 0.0;
     int32_t j = lane;
     constexpr int U = GL::kUnroll;
+    const bool keep = (int64_t)(c - c0) * 100 >= (int64_t)(c1 - c0) * (100 - LARS_K1_KEEP_PCT);
     for (; j + (U - 1) * 32 < ng; j += U * 32) {
       F8 wv[U], gv[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {  // all loads first: 2*U x 32 B in flight per lane
-        wv[u] = ld8_keep(wp + 8 * (j + u * 32));
-        gv[u] = gl.load8(gi + 8 * (j + u * 32));
+        wv[u] = keep ? ld8_keep(wp + 8 * (j + u * 32)) : ld8_nc(wp + 8 * (j + u * 32));
+        gv[u] = gl.load8(gi + 8 * (j + u * 32), keep);
       }
 #pragma unroll
       for (int u = 0; u < U; u += 2) {
@@ -672,8 +666,8 @@ __device__ __forceinline__ void norms_tile(int32_t tile, const DevWork& wk, cons
       }
     }
     for (; j < ng; j += 32) {
-      const F8 w0 = ld8_keep(wp + 8 * j);
-      const F8 g0 = gl.load8(gi + 8 * j);
+      const F8 w0 = keep ? ld8_keep(wp + 8 * j) : ld8_nc(wp + 8 * j);
+      const F8 g0 = gl.load8(gi + 8 * j, keep);
       acc8(aw, w0);
       acc8(ag, g0);
     }
