@@ -22,7 +22,7 @@ constexpr int kThreads = 256;           // threads per CTA of K1 / K2
 #ifndef LARS_NORM_UNROLL
 #define LARS_NORM_UNROLL 2
 #endif
-#ifndef LARS_K1_KEEP_PCT  // carry mode: share of each tile's gradient K1 loads with L2::evict_last
+#ifndef LARS_K1_KEEP_PCT  // share of each tile's fp32 K1 chunk loads (from its end) with L2::evict_last
 #define LARS_K1_KEEP_PCT 100
 #endif
 #ifndef LARS_NORM_UNROLL_G
