@@ -387,6 +387,18 @@ def run_ours(args):
     assert not skipped
     ms_e2e = max_over_ranks(e2.elapsed_time(e3)) / ne
     h2d = h.padded_numel * gbytes
+    # the same bytes as a bare pinned host -> device copy on this box: what the e2e step can at best reach
+    g_dst = torch.empty(g_pin.shape, dtype=g_pin.dtype, device=dev)
+    g_dst.copy_(g_pin, non_blocking=True)
+    torch.cuda.synchronize()
+    e8, e9 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e8.record()
+    for i in range(ne):
+        g_dst.copy_(g_pin, non_blocking=True)
+    e9.record()
+    torch.cuda.synchronize()
+    ms_h2d = max_over_ranks(e8.elapsed_time(e9)) / ne
+    del g_dst
     d2h = 4 + 2 * 8 * (len(lay) if P == 1 else sum(1 for o in h.tensor_owner() if o == rank))
 
     units = P * E
@@ -460,7 +472,8 @@ def run_ours(args):
                            "frac": roof["step_frac_of_bus_roofline"],
                            "note": "reduce-scatter + all-gather bus bytes per rank / whole step time"}),
         "e2e": {"value": round(units / (ms_e2e * 1e-3), 1), "unit": "params/s", "ms_per_step": round(ms_e2e, 4),
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "h2d_copy_ms": round(ms_h2d, 4), "frac_of_h2d_copy": round(ms_h2d / ms_e2e, 4)},
         "clocks": clk,
         "gpu_launches": (2 if fused else 2 if P == 1 else 3) * args.steps,
         "nccl_launches": (3 * args.steps) if (P > 1 and not fused) else 0,
