@@ -381,6 +381,46 @@ def main():
             report["failures"].append(f"host-grad ({'fused' if fused_h else 'nccl'}) differs from device path")
         for hh in hs:
             hh.close()
+    # fused-path handshake stress: a tiny layout (3 tiles, far fewer than F1's grid, so most CTAs leave
+    # without a tile) captured once in a CUDA graph with a device iteration and replayed DP_REPLAYS times
+    # back to back with no host synchronization (the epoch / go / exit-barrier exchange runs every replay);
+    # the result must equal, bit for bit, the same steps issued eagerly with host iterations, on every rank
+    if not sel or re.search(sel, "fused-tiny-graph-replay"):
+        n_rep = int(os.environ.get("DP_REPLAYS", "1000"))
+        lay_s = LY.tiny()
+        kw_s = hp_kwargs(grad_dtype="f16", grad_scale=1.0 / (G.GRAD_PRESCALE * P), flags=1)
+        hs = [PK.Lars([(x.numel, x.kind) for x in lay_s], device=local, nranks=P, **kw_s) for _ in range(2)]
+        pk = lambda hh, a: torch.from_numpy(G.pack(a, hh.offsets, hh.padded_numel).view(a[0].dtype)).to(dev)
+        ws, ms = [], []
+        for hh in hs:
+            hh.comm_init_torch()
+            wsym, gsym = hh.dp_buffers()
+            wsym.copy_(pk(hh, G.weights(lay_s)))
+            gsym.copy_(pk(hh, G.grads(lay_s, rank, 5, "f16")))
+            ws.append(wsym)
+            ms.append(pk(hh, G.momentum(lay_s, 1e-3)))
+            hh.dp_allreduce_lars_step(wsym, gsym, ms[-1], 100)  # eager first step: connections, carried norms
+        torch.cuda.synchronize()
+        it_dev = torch.tensor([101], dtype=torch.int64, device=dev)
+        side = torch.cuda.Stream(device=dev)
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=side, capture_error_mode="thread_local"):
+            hs[0].dp_allreduce_lars_step_dev_iter(ws[0], hs[0].dp_buffers()[1], ms[0], it_dev, stream=side)
+        for _ in range(n_rep):
+            gr.replay()
+        torch.cuda.synchronize()
+        gr.reset()
+        for k in range(n_rep):
+            hs[1].dp_allreduce_lars_step(ws[1], hs[1].dp_buffers()[1], ms[1], 101 + k)
+        torch.cuda.synchronize()
+        same_s = all_same(ws[0])
+        ok_s = (int(it_dev.item()) == 101 + n_rep and torch.equal(ws[0], ws[1]) and torch.equal(ms[0], ms[1])
+                and bool(torch.isfinite(ws[0]).all()) and hs[0].last_step_status() == 0 and same_s)
+        report["cases"].append({"name": "fused-tiny-graph-replay", "replays": n_rep, "bitwise": ok_s})
+        if not ok_s:
+            report["failures"].append("fused graph replays differ from the eager steps (or across ranks)")
+        for hh in hs:
+            hh.close()
     # parallel deterministic initialization: every rank initializes its own replica from
     # the same seed; the replicas are bitwise identical with zero bytes broadcast
     lay_i = LY.resnet50()

@@ -37,6 +37,7 @@ def test_dp_step_parity_and_replica_consistency(nproc, tmp_path):
         names = [c["name"] for c in rep["cases"]]
         assert "r50-f16" in names and "nan-on-rank1" in names and "fused-r50-f16-carry" in names
         assert "fused-overflow-sum-f16" in names and "groups-r50-f16" in names
+        assert "fused-tiny-graph-replay" in names  # 1,000 graph replays of the fused handshake, bitwise
         # fp32 sums (fused path) and P = 1 are gated at the fp32 tolerance
         for c in rep["cases"]:
             if c.get("reduced_dtype") == "f32" or nproc == 1:
