@@ -840,9 +840,23 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_norms_kernel(DevWor
                                                                           const float* __restrict__ w,
                                                                           const void* __restrict__ g,
                                                                           int64_t g_shift) {
-  // wait BEFORE releasing the dependent K2: K2 prefetches w and m before its own wait, so it must not
-  // become resident while the previous step's K2 may still be writing them
+  // wait, then release the dependent K2 (K2 reads only the static work list before its own wait)
   extern __shared__ __align__(128) unsigned char k1_stages[];  // kBulkSmem bytes when BULK
+#if LARS_K1_PREFETCH_LINES > 0
+  // while the previous step's K2 drains: pull the head of each warp's first chunk of g into L2 (the work
+  // list is static; an L2 prefetch cannot go stale, L2 being the device's point of coherence). fp32 only:
+  // for 16-bit gradients it measured slower (profiles/r02_k1_prefetch_sweep.txt)
+  if (!BULK && DT == LARS_F32 && (int32_t)blockIdx.x < wk.ntiles) {
+    const int32_t c = wk.tile_chunk[blockIdx.x] + (int32_t)(threadIdx.x >> 5);
+    if (c < wk.tile_chunk[blockIdx.x + 1]) {
+      const Seg ck = wk.chunks[c];
+      const char* p = (const char*)g + (ck.begin - g_shift) * 4;
+      const int32_t bytes = min(ck.len * 4, LARS_K1_PREFETCH_LINES * 128);
+      for (int32_t o = (int32_t)(threadIdx.x & 31) * 128; o < bytes; o += 32 * 128)
+        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p + o));
+    }
+  }
+#endif
   pdl_wait();
   pdl_trigger();
   TRACE_BEGIN
