@@ -25,6 +25,9 @@ constexpr int kThreads = 256;           // threads per CTA of K1 / K2
 #ifndef LARS_K1_PREFETCH_LINES  // 128-byte lines of each warp's first fp32 g chunk K1 prefetches before its wait
 #define LARS_K1_PREFETCH_LINES 32
 #endif
+#ifndef LARS_K2_PREFETCH_LINES  // 128-byte lines of w and m of each warp's first fp32-g K2 chunk prefetched before its wait
+#define LARS_K2_PREFETCH_LINES 16
+#endif
 #ifndef LARS_K1_KEEP_PCT  // share of each tile's fp32 K1 chunk loads (from its end) with L2::evict_last
 #define LARS_K1_KEEP_PCT 100
 #endif

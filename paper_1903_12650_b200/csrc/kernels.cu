@@ -1200,6 +1200,22 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_update_kernel(DevWo
   static_assert(!(HALF && DEFER), "the deferred finish is the whole-layout step's");
   pdl_trigger();
   if constexpr (DEFER) deferred_prefetch_segs(blockIdx.x, wk);  // static work list: before the wait
+#if LARS_K2_PREFETCH_LINES > 0
+  // while K1 drains: pull the head of w and m of each warp's first chunk (the tile's last) into L2. Both
+  // were last written by the previous K2, complete before K1 passed its own wait and released this grid.
+  // fp32 gradients only: 16-bit measured +0.7 us (profiles/r02_k2_prefetch_sweep.txt)
+  if (!HALF && DT == LARS_F32 && (int32_t)blockIdx.x < wk.ntiles) {
+    const int32_t c = wk.tile_chunk[blockIdx.x + 1] - 1 - (int32_t)(threadIdx.x >> 5);
+    if (c >= wk.tile_chunk[blockIdx.x]) {
+      const Seg ck = wk.chunks[c];
+      const int32_t bytes = min(ck.len * 4, LARS_K2_PREFETCH_LINES * 128);
+      for (int32_t o = (int32_t)(threadIdx.x & 31) * 128; o < bytes; o += 32 * 128) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"((const char*)(w + ck.begin) + o));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"((const char*)(m + ck.begin) + o));
+      }
+    }
+  }
+#endif
   pdl_wait();
   bool skip = false;
   TRACE_BEGIN
