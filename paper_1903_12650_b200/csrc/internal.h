@@ -28,6 +28,9 @@ constexpr int kThreads = 256;           // threads per CTA of K1 / K2
 #ifndef LARS_K2_PREFETCH_LINES  // 128-byte lines of w and m of each warp's first fp32-g K2 chunk prefetched before its wait
 #define LARS_K2_PREFETCH_LINES 16
 #endif
+#ifndef LARS_F2_PREFETCH_LINES  // the same for the fused data-parallel F2 (measured at P = 2)
+#define LARS_F2_PREFETCH_LINES 0
+#endif
 #ifndef LARS_K1_KEEP_PCT  // share of each tile's fp32 K1 chunk loads (from its end) with L2::evict_last
 #define LARS_K1_KEEP_PCT 100
 #endif

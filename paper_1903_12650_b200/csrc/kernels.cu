@@ -1466,6 +1466,21 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) lars_dp_update_gather_ke
   pdl_trigger();
   SplitPre sp;
   if (threadIdx.x < 32) sp = load_split_pre(wk);
+#if LARS_F2_PREFETCH_LINES > 0
+  // while F1 drains: the head of w and m of each warp's first chunk into L2 (as K2; this rank's shard of
+  // w and m is written only by this rank's previous F2, complete before F1 started)
+  if ((int32_t)blockIdx.x < wk.ntiles) {
+    const int32_t c = wk.tile_chunk[blockIdx.x + 1] - 1 - (int32_t)(threadIdx.x >> 5);
+    if (c >= wk.tile_chunk[blockIdx.x]) {
+      const Seg ck = wk.chunks[c];
+      const int32_t bytes = min(ck.len * 4, LARS_F2_PREFETCH_LINES * 128);
+      for (int32_t o = (int32_t)(threadIdx.x & 31) * 128; o < bytes; o += 32 * 128) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"((const char*)(w + ck.begin) + o));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"((const char*)(m + ck.begin) + o));
+      }
+    }
+  }
+#endif
   pdl_wait();  // F1 complete (its shares and reduced shard are visible)
   TRACE_MARK_AT(6, 0)
   if (threadIdx.x < 32) {
